@@ -1,0 +1,122 @@
+/*
+ * menndl_sm100.h — C ABI of libmenndl_sm100.so, the B200 (sm_100a) candidate
+ * evaluation library behind paper_1909_12291_b200.
+ *
+ * The reference (convevo, pure Python + numpy) has no native boundary; the
+ * surfaces this ABI replaces are its Python operator / candidate interfaces:
+ *
+ *   ce_net_create + ce_net_set_params   <- genome.instantiate        (genome.py:309-335)
+ *                                          + nn._kaiming_uniform init (nn.py:44-46)
+ *   ce_train                            <- evaluator.train_short     (evaluator.py:145-171)
+ *                                          looping nn.train_batch    (nn.py:325-331)
+ *   ce_net_train_batch_host             <- nn.train_batch            (nn.py:325-331)
+ *   ce_net_forward_host                 <- nn.Network.forward        (nn.py:264-272)
+ *   ce_net_get_activation               <- per-layer outputs of Conv2d/ReLU/MaxPool/Dense.forward
+ *                                          (nn.py:82-94, 140-150, 178-180, 225-231)
+ *   ce_net_get_grads                    <- Layer.grads after Network.backward (nn.py:96-116, 233-240)
+ *   ce_net_get_params                   <- Layer.params / Layer._vel after sgd_step (nn.py:306-322)
+ *   ce_predict                          <- evaluator.predict_scores  (evaluator.py:174-186)
+ *   ce_latency                          <- evaluator.measure_latency (evaluator.py:189-210)
+ *   ce_dataset_create                   <- data.PatchSet.as_float    (data.py:65-66), uploaded once
+ *
+ * Conventions
+ *   - Every entry point returns a status (CE_OK ... CE_ECUDA); the message of
+ *     the last failure on the calling thread is available from ce_last_error().
+ *     Python maps CE_EINVAL -> ShapeError/ValueError, everything else ->
+ *     EvalFailure (errors.py:4-26), so no exception escapes evaluate().
+ *   - Host pointers are never retained after a call returns. A ce_net owns its
+ *     device buffers; one ce_net is used by one thread at a time; distinct nets
+ *     may be driven concurrently from different threads (different streams).
+ *   - Host-side tensors use the reference layouts: activations NCHW float32,
+ *     conv weights (out, in, kh, kw), dense weights (out, in) with the flatten
+ *     order (c, h, w) of nn.Flatten (nn.py:197-199). Device layouts are NHWC
+ *     and are converted inside the library.
+ */
+#ifndef MENNDL_SM100_H
+#define MENNDL_SM100_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define CE_OK 0
+#define CE_EINVAL 1     /* bad argument / shape            -> ShapeError / ValueError */
+#define CE_ENONFINITE 2 /* non-finite loss                 -> EvalFailure             */
+#define CE_ENOMEM 3     /* device allocation failed        -> EvalFailure             */
+#define CE_ECUDA 4      /* CUDA launch / runtime failure   -> EvalFailure (+ GPU unhealthy if sticky) */
+
+/* precision of activations and conv/dense operands */
+#define CE_PREC_BF16 0 /* bf16 operands, fp32 accumulate, fp32 master weights (tcgen05 path) */
+#define CE_PREC_FP32 1 /* fp32 check mode (CUDA-core FFMA)                                   */
+
+/* layer kinds of a network descriptor (ReLU is a flag on conv, Flatten is implicit) */
+#define CE_LAYER_CONV 1
+#define CE_LAYER_POOL 2
+#define CE_LAYER_DENSE 3
+
+typedef struct ce_layer_desc {
+  int kind;         /* CE_LAYER_*                                    */
+  int out_channels; /* conv                                          */
+  int kernel;       /* conv kernel / pool window                     */
+  int stride;       /* conv / pool stride                            */
+  int relu;         /* conv: ReLU follows (genome.py:322-323)        */
+  int units;        /* dense output units                            */
+} ce_layer_desc;
+
+typedef struct ce_net_desc {
+  int in_c, in_h, in_w;        /* per-sample input shape (3, 100, 100)          */
+  int n_layers;                /* feature layers, then dense layers (last = classes) */
+  const ce_layer_desc* layers;
+  int max_batch;               /* largest batch the net will see               */
+} ce_net_desc;
+
+typedef struct ce_net ce_net;
+typedef struct ce_dataset ce_dataset;
+
+int ce_version(void);
+const char* ce_last_error(void);
+int ce_device_count(int* count);
+
+/* ---- datasets: u8 NCHW pixels + u8 labels, uploaded once per device ------ */
+int ce_dataset_create(int device, const uint8_t* pixels, const uint8_t* labels, int n, int c, int h, int w,
+                      ce_dataset** out);
+int ce_dataset_destroy(ce_dataset* ds);
+
+/* ---- networks ------------------------------------------------------------- */
+int ce_net_create(const ce_net_desc* desc, int device, int precision, ce_net** out);
+int ce_net_destroy(ce_net* net);
+/* bytes of device memory the net holds (parameters + activations + workspace) */
+int ce_net_device_bytes(const ce_net* net, size_t* bytes);
+/* number of parameterised layers (conv + dense), in layer order */
+int ce_net_num_param_layers(const ce_net* net, int* count);
+/* param layer p: weights in reference layout (conv (o,c,kh,kw), dense (o,in)), bias (o) */
+int ce_net_set_params(ce_net* net, int p, const float* w, const float* b);
+int ce_net_get_params(ce_net* net, int p, float* w, float* b, float* vel_w, float* vel_b);
+int ce_net_get_grads(ce_net* net, int p, float* gw, float* gb);
+
+/* inference forward of n samples (float32 NCHW host) -> logits (n, classes) */
+int ce_net_forward_host(ce_net* net, const float* x, int n, float* logits);
+/* output of layer `layer` (descriptor index) from the last forward, NCHW / (n, units) float32 */
+int ce_net_get_activation(ce_net* net, int layer, int n, float* out);
+/* one SGD step on a host batch; writes the pre-step mean loss */
+int ce_net_train_batch_host(ce_net* net, const float* x, const int64_t* labels, int n, float lr, float momentum,
+                            float* loss);
+
+/* train_short: `epochs` x `steps_per_epoch` steps of batch max_batch; perm is
+ * epochs x n_train int32 (one numpy permutation per epoch). losses receives one
+ * pre-step loss per step. device_ms receives the device time of the loop.   */
+int ce_train(ce_net* net, const ce_dataset* train, const int32_t* perm, int epochs, int steps_per_epoch, float lr,
+             float momentum, float* losses, double* device_ms);
+/* predict_scores: softmax p[:,1] and argmax over the whole set in chunks of `batch` */
+int ce_predict(ce_net* net, const ce_dataset* set, int batch, double* scores, int64_t* preds);
+/* measure_latency: warmup + reps device-timed forwards of a host batch (float32 NCHW) */
+int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MENNDL_SM100_H */

@@ -1,0 +1,251 @@
+// Warp-specialised tcgen05 implicit-GEMM engine (sm_100a, cta_group::1).
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]     (bf16 operands, fp32 accumulate in TMEM)
+//
+// The engine knows nothing about convolutions: a Loader policy gathers 16-byte
+// chunks of A and B for one (tile, k-block) into shared memory with cp.async
+// (zero-fill for padding / invalid taps), and an Epilogue policy consumes the
+// fp32 accumulator rows. Roles per CTA (persistent, grid <= #SMs):
+//
+//   warps 0-3  producers: cp.async gather into an S-stage smem ring
+//   warps 4-7  epilogue : tcgen05.ld TMEM -> registers -> Epilogue::store
+//   warp  8    MMA      : TMEM alloc + one elected thread issuing tcgen05.mma
+//
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile t overlap the
+// MMAs of tile t+1. Shared-memory tiles use the SWIZZLE_NONE canonical layouts
+// (see ptx.cuh::make_sdesc): a stage holds A as [kchunk][128 rows][16 B] and B
+// as [kchunk][BN rows][16 B] (K-major) or the MN-major analogue.
+#pragma once
+#include "ptx.cuh"
+
+namespace ce {
+
+constexpr int TC_BM = 128;  // UMMA M (rows per tile = TMEM lanes)
+constexpr int TC_BK = 64;   // K elements per pipeline stage (8 x 16-byte chunks)
+constexpr int TC_PRODUCERS = 128;
+constexpr int TC_THREADS = 288;
+constexpr int TC_LAG = 2;  // cp.async groups kept in flight before signalling
+
+// Tile coordinates handed to loaders / epilogues.
+struct TileCoord {
+  int m0;     // first row of the tile
+  int n0;     // first column (output channel) of the tile
+  int split;  // reduction split index
+  int kb0;    // first k-block of this split
+  int nkb;    // number of k-blocks of this split
+};
+
+struct TcShape {
+  int M, N;          // problem rows / columns
+  int K;             // reduction length (elements)
+  int m_tiles, n_tiles, splits;
+  int kb_per_split;  // k-blocks per split (last split may have fewer)
+};
+
+__host__ __device__ inline TcShape tc_make_shape(int M, int N, int K, int BN, int splits) {
+  TcShape s;
+  s.M = M;
+  s.N = N;
+  s.K = K;
+  s.m_tiles = (M + TC_BM - 1) / TC_BM;
+  s.n_tiles = (N + BN - 1) / BN;
+  int nkb = (K + TC_BK - 1) / TC_BK;
+  if (splits < 1) splits = 1;
+  if (splits > nkb) splits = nkb;
+  s.kb_per_split = (nkb + splits - 1) / splits;
+  s.splits = (nkb + s.kb_per_split - 1) / s.kb_per_split;
+  return s;
+}
+
+__device__ inline TileCoord tc_tile(const TcShape& s, int t, int bn) {
+  TileCoord c;
+  int per_split = s.m_tiles * s.n_tiles;
+  c.split = t / per_split;
+  int r = t - c.split * per_split;
+  int nt = r / s.m_tiles;
+  int mt = r - nt * s.m_tiles;
+  c.m0 = mt * TC_BM;
+  c.n0 = nt * bn;
+  int nkb = (s.K + TC_BK - 1) / TC_BK;
+  c.kb0 = c.split * s.kb_per_split;
+  int end = c.kb0 + s.kb_per_split;
+  if (end > nkb) end = nkb;
+  c.nkb = end - c.kb0;
+  return c;
+}
+
+template <int BN>
+struct TcSmemLayout {
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
+  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + alignment slack
+};
+
+template <int BN, class Loader, class Epi>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ Loader ld, const __grid_constant__ Epi epi, const TcShape shape) {
+  using L = TcSmemLayout<BN>;
+  constexpr int S = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + S * L::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_base_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int total_tiles = shape.m_tiles * shape.n_tiles * shape.splits;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], TC_PRODUCERS);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 8) tmem_alloc(tmem_base_slot, L::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+  const uint32_t smem_base = smem_u32(smem);
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ producers
+    const int ptid = threadIdx.x;
+    int stage = 0;
+    uint32_t phase = 0;
+    int pending_stage[TC_LAG + 1];
+    int npending = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      TileCoord c = tc_tile(shape, t, BN);
+      for (int kb = 0; kb < c.nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
+        const uint32_t sB = sA + L::A_BYTES;
+        ld.load(c, c.kb0 + kb, sA, sB, ptid);
+        cp_async_commit();
+        // retire the oldest group once TC_LAG newer ones are in flight
+        if (npending == TC_LAG) {
+          cp_async_wait<TC_LAG>();
+          fence_proxy_async();
+          mbar_arrive(&full[pending_stage[0]]);
+          for (int i = 0; i < TC_LAG - 1; ++i) pending_stage[i] = pending_stage[i + 1];
+          --npending;
+        }
+        pending_stage[npending++] = stage;
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    cp_async_wait_all();
+    fence_proxy_async();
+    for (int i = 0; i < npending; ++i) mbar_arrive(&full[pending_stage[i]]);
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp - 4;  // TMEM lane quarter (warp % 4 == q)
+    const int row_in_tile = q * 32 + lane;
+    int lt = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++lt) {
+      TileCoord c = tc_tile(shape, t, BN);
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int col = 0; col < BN; col += 16) {
+        uint32_t r[16];
+        tmem_ld16(tbase + col, r);
+        tmem_ld_wait();
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        epi.store(c, row_in_tile, col, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    epi.finish(lane, q);
+  } else {
+    // ------------------------------------------------------------ MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int lt = 0;
+    constexpr uint32_t idesc = make_idesc_bf16(TC_BM, BN, Loader::A_MN_MAJOR, Loader::B_MN_MAJOR);
+    const int k16_total = (shape.K + 15) / 16;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++lt) {
+      TileCoord c = tc_tile(shape, t, BN);
+      const int acc = lt & 1;
+      mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < c.nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
+          const uint32_t sB = sA + L::A_BYTES;
+          const int gkb = c.kb0 + kb;
+          int nk16 = k16_total - gkb * (TC_BK / 16);
+          if (nk16 > TC_BK / 16) nk16 = TC_BK / 16;
+#pragma unroll 1
+          for (int k = 0; k < nk16; ++k) {
+            // K-major: a K=16 step covers chunks 2k, 2k+1 (LBO apart).
+            // MN-major: a K=16 step covers K groups 2k, 2k+1 (LBO apart).
+            const uint64_t ad = make_sdesc(sA + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
+            const uint64_t bd = make_sdesc(sB + (uint32_t)(2 * k) * (BN * 16), BN * 16, 128);
+            umma_bf16(d_tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (kb == c.nkb - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, L::TMEM_COLS);
+  }
+}
+
+// Byte offset of a 16-byte chunk inside a stage tile with R rows.
+//   K-major : chunk (row r, kchunk kc)          -> (kc * R + r) * 16
+//   MN-major: chunk (MN group g, k index kk)    -> (kk/8) * R*16 + g*128 + (kk%8)*16
+__device__ __forceinline__ uint32_t kmajor_off(int R, int r, int kc) { return (uint32_t)(kc * R + r) * 16u; }
+__device__ __forceinline__ uint32_t mnmajor_off(int R, int g, int kk) {
+  return (uint32_t)((kk >> 3) * R * 16 + g * 128 + (kk & 7) * 16);
+}
+
+template <int BN, class Loader, class Epi>
+inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& shape, int num_sms, cudaStream_t st) {
+  using L = TcSmemLayout<BN>;
+  auto kern = tc_gemm_kernel<BN, Loader, Epi>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+  if (e != cudaSuccess) return e;
+  int tiles = shape.m_tiles * shape.n_tiles * shape.splits;
+  int grid = tiles < num_sms ? tiles : num_sms;
+  if (grid < 1) grid = 1;
+  kern<<<grid, TC_THREADS, L::TOTAL, st>>>(ld, epi, shape);
+  return cudaGetLastError();
+}
+
+}  // namespace ce
