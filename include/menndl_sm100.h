@@ -106,11 +106,14 @@ int ce_net_get_activation(ce_net* net, int layer, int n, float* out);
 int ce_net_train_batch_host(ce_net* net, const float* x, const int64_t* labels, int n, float lr, float momentum,
                             float* loss);
 
-/* train_short: `epochs` x `steps_per_epoch` steps of batch max_batch; perm is
- * epochs x n_train int32 (one numpy permutation per epoch). losses receives one
- * pre-step loss per step. device_ms receives the device time of the loop.   */
-int ce_train(ce_net* net, const ce_dataset* train, const int32_t* perm, int epochs, int steps_per_epoch, float lr,
-             float momentum, float* losses, double* device_ms);
+/* train_short: `epochs` x `steps_per_epoch` steps of `batch` samples; perm is
+ * epochs x n_perm int32 (one numpy permutation of the n_perm training patches
+ * per epoch, evaluator.py:161); step b of an epoch uses perm[b*batch:(b+1)*batch]
+ * (evaluator.py:139-142). losses receives one pre-step loss per step (the
+ * caller raises EvalFailure at the first non-finite one, evaluator.py:168-170);
+ * device_ms receives the device time of the loop.                            */
+int ce_train(ce_net* net, const ce_dataset* train, const int32_t* perm, int n_perm, int epochs,
+             int steps_per_epoch, int batch, float lr, float momentum, float* losses, double* device_ms);
 /* predict_scores: softmax p[:,1] and argmax over the whole set in chunks of `batch` */
 int ce_predict(ce_net* net, const ce_dataset* set, int batch, double* scores, int64_t* preds);
 /* measure_latency: warmup + reps device-timed forwards of a host batch (float32 NCHW) */

@@ -1,0 +1,296 @@
+// Convolution forward / dgrad / wgrad as implicit GEMMs on the tcgen05 engine.
+//
+// All three passes put a channel count on the UMMA N axis (<= 256, so one N
+// tile per problem) and gather 16-byte chunks of 8 consecutive channels:
+//
+//   fwd  : D[(n,p,q)][o]  = sum_{(i,j,c)} x[n, sp+i, sq+j, c] * W[o][i][j][c]      A,B K-major
+//          epilogue: + bias, ReLU, bf16 NHWC store                 (nn.py:82-94, 178-180)
+//   dgrad: D[(n,h,w)][c]  = sum_{(i,j,o)} dy[n, (h-i)/s, (w-j)/s, o] * Wt[c][i][j][o]   A,B K-major
+//          invalid taps (not on the stride lattice / out of range) are zero-filled;
+//          epilogue: x ReLU mask of the input activation, bf16 store  (nn.py:112-113, 183)
+//   wgrad: D[(i,j,c)][o]  = sum_{(n,p,q)} x[n, sp+i, sq+j, c] * dy[n,p,q,o]           A,B MN-major
+//          reduction split across CTAs; epilogue writes fp32 partials part[split][o][(i,j,c)]
+//          that conv_sgd_kernel reduces in fixed order and feeds to the momentum update
+//          (nn.py:108-115, 306-322)
+#pragma once
+#include <cstdlib>
+#include "tc_engine.cuh"
+#include "kernels.cuh"
+
+namespace ce {
+
+inline bool conv_tc_enabled() {
+  const char* e = getenv("CE_DISABLE_TC");
+  return !(e && e[0] == '1');
+}
+
+// ------------------------------------------------------------------ forward
+struct FwdTcLoader {
+  static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  const bf16* x;
+  const bf16* w;  // [o][K]
+  ConvGeom g;
+  int K, M, BN;
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid) const {
+    // A: this thread owns row r = ptid of the tile (128 rows, 128 producers)
+    {
+      const int r = ptid;
+      const int m = c.m0 + r;
+      const bool row_ok = m < M;
+      int q = 0, p = 0, n = 0;
+      if (row_ok) {
+        q = m % g.ow;
+        int t = m / g.ow;
+        p = t % g.oh;
+        n = t / g.oh;
+      }
+      const bf16* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {
+        const int kk = kb * TC_BK + kc * 8;
+        const bool ok = row_ok && kk < K;
+        const bf16* src = x;
+        if (ok) {
+          const int tap = kk / g.c, c0 = kk - tap * g.c;
+          const int i = tap / g.k, j = tap - i * g.k;
+          src = base + ((size_t)i * g.w + j) * g.c + c0;
+        }
+        cp_async16(sA + kmajor_off(TC_BM, r, kc), src, ok ? 16u : 0u);
+      }
+    }
+    // B: weights, BN rows x 8 chunks
+    for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
+      const int r = ch % BN, kc = ch / BN;
+      const int o = c.n0 + r, kk = kb * TC_BK + kc * 8;
+      const bool ok = o < g.co && kk < K;
+      cp_async16(sB + kmajor_off(BN, r, kc), ok ? (const void*)(w + (size_t)o * K + kk) : (const void*)w,
+                 ok ? 16u : 0u);
+    }
+  }
+};
+
+struct FwdTcEpi {
+  bf16* y;
+  const float* bias;
+  int M, co, relu;
+  __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
+    const int m = c.m0 + row;
+    const int o0 = c.n0 + col;
+    if (m >= M || o0 >= co) return;
+    bf16* dst = y + (size_t)m * co + o0;
+    __align__(16) bf16 out[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float t = v[i] + (o0 + i < co ? bias[o0 + i] : 0.f);
+      if (relu) t = t > 0.f ? t : 0.f;
+      out[i] = __float2bfloat16_rn(t);
+    }
+    *(uint4*)dst = *(const uint4*)&out[0];
+    if (o0 + 8 < co) *(uint4*)(dst + 8) = *(const uint4*)&out[8];
+  }
+  __device__ void finish(int, int) const {}
+};
+
+// ------------------------------------------------------------------ dgrad
+struct DgradTcLoader {
+  static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  const bf16* dy;
+  const bf16* wt;  // [c][k*k*co]
+  ConvGeom g;
+  int K, M, BN;
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid) const {
+    {
+      const int r = ptid;
+      const int m = c.m0 + r;
+      const bool row_ok = m < M;
+      int wx = 0, hy = 0, n = 0;
+      if (row_ok) {
+        wx = m % g.w;
+        int t = m / g.w;
+        hy = t % g.h;
+        n = t / g.h;
+      }
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {
+        const int kk = kb * TC_BK + kc * 8;
+        bool ok = row_ok && kk < K;
+        const bf16* src = dy;
+        if (ok) {
+          const int tap = kk / g.co, o0 = kk - tap * g.co;
+          const int i = tap / g.k, j = tap - i * g.k;
+          int hp = hy - i, wq = wx - j;
+          ok = hp >= 0 && wq >= 0 && (hp % g.s) == 0 && (wq % g.s) == 0;
+          hp /= g.s;
+          wq /= g.s;
+          ok = ok && hp < g.oh && wq < g.ow;
+          if (ok) src = dy + (((size_t)n * g.oh + hp) * g.ow + wq) * g.co + o0;
+        }
+        cp_async16(sA + kmajor_off(TC_BM, r, kc), src, ok ? 16u : 0u);
+      }
+    }
+    for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
+      const int r = ch % BN, kc = ch / BN;
+      const int cc = c.n0 + r, kk = kb * TC_BK + kc * 8;
+      const bool ok = cc < g.c && kk < K;
+      cp_async16(sB + kmajor_off(BN, r, kc), ok ? (const void*)(wt + (size_t)cc * K + kk) : (const void*)wt,
+                 ok ? 16u : 0u);
+    }
+  }
+};
+
+struct DgradTcEpi {
+  bf16* dx;
+  const bf16* mask;
+  int M, c;
+  __device__ void store(const TileCoord& tc, int row, int col, const float (&v)[16]) const {
+    const int m = tc.m0 + row;
+    const int c0 = tc.n0 + col;
+    if (m >= M || c0 >= c) return;
+    const size_t off = (size_t)m * c + c0;
+    __align__(16) bf16 out[16];
+    __align__(16) bf16 mk[16];
+    if (mask) {
+      *(uint4*)&mk[0] = *(const uint4*)(mask + off);
+      if (c0 + 8 < c) *(uint4*)&mk[8] = *(const uint4*)(mask + off + 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float t = v[i];
+      if (mask && !(__bfloat162float(mk[i]) > 0.f)) t = 0.f;
+      out[i] = __float2bfloat16_rn(t);
+    }
+    *(uint4*)(dx + off) = *(const uint4*)&out[0];
+    if (c0 + 8 < c) *(uint4*)(dx + off + 8) = *(const uint4*)&out[8];
+  }
+  __device__ void finish(int, int) const {}
+};
+
+// ------------------------------------------------------------------ wgrad
+struct WgradTcLoader {
+  static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
+  const bf16* x;
+  const bf16* dy;
+  ConvGeom g;
+  int Kf;  // k*k*c (rows of D)
+  int Mo;  // reduction length n*oh*ow
+  int BN;
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid) const {
+    // A: 16 groups of 8 (i,j,c) rows x 64 reduction indices
+    {
+      const int grp = ptid & 15;
+      const int kk0 = c.m0 + grp * 8;
+      const bool grp_ok = kk0 < Kf;
+      int tap_off = 0;
+      if (grp_ok) {
+        const int tap = kk0 / g.c, c0 = kk0 - tap * g.c;
+        const int i = tap / g.k, j = tap - i * g.k;
+        tap_off = (i * g.w + j) * g.c + c0;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int kr = (ptid >> 4) + e * 8;  // 0..63
+        const int m = kb * TC_BK + kr;
+        const bool ok = grp_ok && m < Mo;
+        const bf16* src = x;
+        if (ok) {
+          const int q = m % g.ow;
+          const int t = m / g.ow;
+          const int p = t % g.oh, n = t / g.oh;
+          src = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c + tap_off;
+        }
+        cp_async16(sA + mnmajor_off(TC_BM, grp, kr), src, ok ? 16u : 0u);
+      }
+    }
+    // B: BN/8 groups of 8 output channels x 64 reduction indices
+    const int groups = BN / 8;
+    for (int ch = ptid; ch < groups * TC_BK; ch += TC_PRODUCERS) {
+      const int grp = ch % groups, kr = ch / groups;
+      const int o0 = c.n0 + grp * 8, m = kb * TC_BK + kr;
+      const bool ok = o0 < g.co && m < Mo;
+      cp_async16(sB + mnmajor_off(BN, grp, kr), ok ? (const void*)(dy + (size_t)m * g.co + o0) : (const void*)dy,
+                 ok ? 16u : 0u);
+    }
+  }
+};
+
+struct WgradTcEpi {
+  float* part;  // [split][co][Kf]
+  int Kf, co;
+  __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
+    const int kk = c.m0 + row;
+    if (kk >= Kf) return;
+    float* base = part + (size_t)c.split * co * Kf + kk;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int o = c.n0 + col + i;
+      if (o < co) base[(size_t)o * Kf] = v[i];
+    }
+  }
+  __device__ void finish(int, int) const {}
+};
+
+// ------------------------------------------------------------------ dispatch
+template <class Fn>
+inline int with_bn(int n, Fn&& fn) {
+  if (n <= 16) return fn(std::integral_constant<int, 16>());
+  if (n <= 32) return fn(std::integral_constant<int, 32>());
+  if (n <= 64) return fn(std::integral_constant<int, 64>());
+  if (n <= 128) return fn(std::integral_constant<int, 128>());
+  return fn(std::integral_constant<int, 256>());
+}
+
+inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const float* bias, int relu, bf16* y,
+                       int num_sms, cudaStream_t st) {
+  const int M = g.n * g.oh * g.ow, K = g.k * g.k * g.c;
+  return with_bn(g.co, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
+    FwdTcLoader ld{x, w, g, K, M, BN};
+    FwdTcEpi ep{y, bias, M, g.co, relu};
+    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc: %s", cudaGetErrorString(e));
+  });
+}
+
+inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, const bf16* mask, bf16* dx, int num_sms,
+                         cudaStream_t st) {
+  const int M = g.n * g.h * g.w, K = g.k * g.k * g.co;
+  return with_bn(g.c, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
+    DgradTcLoader ld{dy, wt, g, K, M, BN};
+    DgradTcEpi ep{dx, mask, M, g.c};
+    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_dgrad_tc: %s", cudaGetErrorString(e));
+  });
+}
+
+inline int conv_wgrad_splits(const ConvGeom& g, int n, int num_sms) {
+  const int Kf = g.k * g.k * g.c;
+  const long long Mo = (long long)n * g.oh * g.ow;
+  const int m_tiles = (Kf + TC_BM - 1) / TC_BM;
+  const long long nkb = (Mo + TC_BK - 1) / TC_BK;
+  long long want = (num_sms + m_tiles - 1) / m_tiles;
+  if (want > nkb / 4) want = nkb / 4;  // at least 4 k-blocks per split
+  if (want > 128) want = 128;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+inline int conv_wgrad_tc_max_splits(const ConvGeom& g, int n, int num_sms) { return conv_wgrad_splits(g, n, num_sms); }
+
+inline int conv_wgrad_tc(const ConvGeom& g, const bf16* x, const bf16* dy, float* part, int* splits_out, int num_sms,
+                         cudaStream_t st) {
+  const int Kf = g.k * g.k * g.c, Mo = g.n * g.oh * g.ow;
+  const int want = conv_wgrad_splits(g, g.n, num_sms);
+  return with_bn(g.co, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(Kf, g.co, Mo, BN, want);
+    *splits_out = sh.splits;
+    WgradTcLoader ld{x, dy, g, Kf, Mo, BN};
+    WgradTcEpi ep{part, Kf, g.co};
+    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_wgrad_tc: %s", cudaGetErrorString(e));
+  });
+}
+
+}  // namespace ce

@@ -1,0 +1,840 @@
+// Candidate runtime behind the C ABI (include/menndl_sm100.h).
+//
+// A ce_net is one instantiated genome on one device: parameters (fp32 master
+// weights + momentum, bf16 mirrors for the tensor-core path), per-layer
+// activations for backward, ping-pong gradient buffers and a split-K
+// workspace. ce_train captures one training step (gather -> forward -> xent ->
+// backward + fused SGD) into a CUDA graph and replays it; a device step counter
+// selects the permutation slice and loss slot, so the whole budget runs without
+// host round trips (evaluator.py:160-170 in one call).
+#include <cstdarg>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+#include <cmath>
+#include "ops.cuh"
+#include "conv_tc.cuh"
+
+namespace ce {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+struct Layer {
+  int kind = 0, relu = 0;
+  ConvGeom g{};          // conv / pool geometry (n set per launch)
+  int c_real = 0;        // real channels of the input (first layer: 3 of 8 stored)
+  int out_c_store = 0, out_c_real = 0;
+  int in_units = 0, out_units = 0;  // dense (in_units = stored flat width)
+  int hw_in = 0;         // dense after features: h*w of the flattened input
+  bool in_is_act = true; // dense: input is a T activation (features / image), else fp32 dense output
+  bool need_dx = false, mask_in = false;
+  int pidx = -1;
+  float *W = nullptr, *b = nullptr, *VW = nullptr, *Vb = nullptr, *GW = nullptr, *Gb = nullptr;
+  bf16 *Wbf = nullptr, *Wtbf = nullptr;
+  size_t wn = 0;
+  int bn = 0;
+  void* out = nullptr;
+  uint8_t* arg = nullptr;
+  size_t out_per_sample = 0;  // elements
+};
+
+}  // namespace ce
+
+using namespace ce;
+
+struct ce_dataset {
+  int device = 0;
+  uint8_t* pix = nullptr;
+  uint8_t* lab = nullptr;
+  int n = 0, c = 0, h = 0, w = 0;
+};
+
+struct ce_net {
+  int device = 0, prec = CE_PREC_BF16, num_sms = 148;
+  cudaStream_t st = nullptr;
+  int in_c = 3, in_cp = 8, in_h = 100, in_w = 100, max_batch = 0, classes = 2;
+  std::vector<Layer> L;
+  std::vector<int> params;
+  void* x0 = nullptr;
+  int32_t* ybatch = nullptr;
+  void* gbuf[2] = {nullptr, nullptr};
+  size_t gbytes = 0;
+  float* ws = nullptr;
+  size_t ws_bytes = 0;
+  int* d_step = nullptr;
+  float* d_losses = nullptr;
+  int losses_cap = 0;
+  int32_t* d_perm = nullptr;
+  size_t perm_cap = 0;
+  double* d_scores = nullptr;
+  int64_t* d_preds = nullptr;
+  size_t pred_cap = 0;
+  float* d_xhost = nullptr;
+  size_t xhost_cap = 0;
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  bool keep_grads = false;
+  bool use_tc = false;
+};
+
+namespace {
+
+int dev_alloc(ce_net* net, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~(size_t)255;
+  cudaError_t e = cudaMallocAsync(p, bytes, net->st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CE_ENOMEM, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  }
+  net->allocs.push_back(*p);
+  net->bytes += bytes;
+  return CE_OK;
+}
+#define ALLOC(ptr, bytes)                                             \
+  do {                                                                \
+    int s_ = dev_alloc(net, (void**)&(ptr), (bytes));                 \
+    if (s_ != CE_OK) return s_;                                       \
+  } while (0)
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DevGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline size_t act_bytes(const ce_net* net) { return net->prec == CE_PREC_FP32 ? 4 : 2; }
+
+int pick_splits(long long blocks_per_split, long long K, long long min_chunk, int num_sms) {
+  long long want = (2LL * num_sms + blocks_per_split - 1) / blocks_per_split;
+  long long cap = K / min_chunk;
+  if (want > cap) want = cap;
+  if (want > 64) want = 64;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+// ----------------------------------------------------------------------------- forward
+template <class T>
+int enqueue_forward(ce_net* net, int n) {
+  cudaStream_t st = net->st;
+  const void* in = net->x0;
+  bool in_act = true;
+  for (size_t li = 0; li < net->L.size(); ++li) {
+    Layer& l = net->L[li];
+    if (l.kind == CE_LAYER_CONV) {
+      ConvGeom g = l.g;
+      g.n = n;
+      const int M = n * g.oh * g.ow, K = g.k * g.k * g.c;
+      if (net->use_tc) {
+        int s = conv_fwd_tc(g, (const bf16*)in, l.Wbf, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
+        if (s != CE_OK) return s;
+      } else {
+        simt_gemm(FwdA<T>{(const T*)in, g}, FwdB{l.W, K}, FwdEpi<T>{(T*)l.out, l.b, g.co, l.relu != 0}, M, g.co, K,
+                  1, st);
+      }
+    } else if (l.kind == CE_LAYER_POOL) {
+      ConvGeom g = l.g;
+      g.n = n;
+      size_t total = (size_t)n * g.oh * g.ow * g.c;
+      maxpool_fwd_kernel<T><<<grid_for(total), 256, 0, st>>>((const T*)in, g, (T*)l.out, l.arg);
+    } else {
+      const int B = n, K = l.in_units, O = l.out_units;
+      long long bps = (long long)cdiv(B, SG_BM) * cdiv(O, SG_BN);
+      int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms));
+      PartialEpi pe{net->ws, B, O};
+      if (in_act)
+        simt_gemm(DenseXA<T>{(const T*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
+      else
+        simt_gemm(DenseXA<float>{(const float*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
+      dense_reduce_kernel<<<grid_for((size_t)B * O), 256, 0, st>>>(net->ws, splits, B, O, l.b, (float*)l.out);
+    }
+    CE_CHECK_LAUNCH();
+    in = l.out;
+    in_act = l.kind != CE_LAYER_DENSE;
+  }
+  return CE_OK;
+}
+
+template <class TO, class TM>
+struct DenseDxEpi {
+  TO* dx;
+  const TM* mask;
+  int in;
+  __device__ void operator()(int b, int i, int, float v) const {
+    size_t off = (size_t)b * in + i;
+    if (mask && !(ldf(mask, off) > 0.f)) v = 0.f;
+    stf(dx, off, v);
+  }
+};
+
+// ----------------------------------------------------------------------------- backward + SGD
+template <class T>
+int enqueue_backward(ce_net* net, int n, float lr, float mu) {
+  cudaStream_t st = net->st;
+  int cur = 0;  // gbuf[cur] holds dL/d(output of layer li) (pre-ReLU for conv)
+  const bool keep = net->keep_grads;
+  for (int li = (int)net->L.size() - 1; li >= 0; --li) {
+    Layer& l = net->L[li];
+    const void* x = li == 0 ? net->x0 : net->L[li - 1].out;
+    const void* gin = net->gbuf[cur];
+    void* gout = net->gbuf[cur ^ 1];
+    const T* mask = (l.mask_in && li > 0) ? (const T*)net->L[li - 1].out : nullptr;
+    if (l.kind == CE_LAYER_DENSE) {
+      const int B = n, K = l.in_units, O = l.out_units;
+      const float* g = (const float*)gin;
+      if (l.need_dx) {
+        if (l.in_is_act)
+          simt_gemm(DenseGA{g, O}, DenseWN{l.W, K}, DenseDxEpi<T, T>{(T*)gout, mask, K}, B, K, O, 1, st);
+        else
+          simt_gemm(DenseGA{g, O}, DenseWN{l.W, K}, DenseDxEpi<float, float>{(float*)gout, nullptr, K}, B, K, O, 1,
+                    st);
+        CE_CHECK_LAUNCH();
+      }
+      DenseSgdEpi se{l.W, l.VW, keep ? l.GW : nullptr, nullptr, K, lr, mu};
+      if (l.in_is_act)
+        simt_gemm(DenseGT{g, O}, DenseXN<T>{(const T*)x, K}, se, O, K, B, 1, st);
+      else
+        simt_gemm(DenseGT{g, O}, DenseXN<float>{(const float*)x, K}, se, O, K, B, 1, st);
+      CE_CHECK_LAUNCH();
+      float* bpart = net->ws;
+      colsum_partial_kernel<float><<<dim3(cdiv(O, 256), 1), 256, 0, st>>>(g, B, O, B, bpart);
+      bias_sgd_kernel<<<cdiv(O, 256), 256, 0, st>>>(bpart, 1, O, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
+      CE_CHECK_LAUNCH();
+    } else if (l.kind == CE_LAYER_CONV) {
+      ConvGeom g = l.g;
+      g.n = n;
+      const T* dy = (const T*)gin;
+      const int Mo = n * g.oh * g.ow, K = g.k * g.k * g.c;
+      if (l.need_dx) {
+        if (net->use_tc) {
+          int s = conv_dgrad_tc(g, (const bf16*)dy, l.Wtbf, (const bf16*)mask, (bf16*)gout, net->num_sms, st);
+          if (s != CE_OK) return s;
+        } else {
+          simt_gemm(DgradA<T>{dy, g}, DgradB{l.W, g}, DgradEpi<T>{(T*)gout, mask, g.c}, n * g.h * g.w, g.c,
+                    g.k * g.k * g.co, 1, st);
+        }
+        CE_CHECK_LAUNCH();
+      }
+      int splits;
+      if (net->use_tc) {
+        int s = conv_wgrad_tc(g, (const bf16*)x, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
+        if (s != CE_OK) return s;
+      } else {
+        long long bps = (long long)cdiv(g.co, SG_BM) * cdiv(K, SG_BN);
+        splits = simt_splits(Mo, pick_splits(bps, Mo, 512, net->num_sms));
+        simt_gemm(WgradA<T>{dy, g.co}, WgradB<T>{FwdA<T>{(const T*)x, g}}, PartialEpi{net->ws, g.co, K}, g.co, K, Mo,
+                  splits, st);
+      }
+      CE_CHECK_LAUNCH();
+      float* bpart = net->ws + (size_t)splits * g.co * K;
+      int bsplits = std::min(64, std::max(1, Mo / 2048));
+      int mchunk = cdiv(Mo, bsplits);
+      colsum_partial_kernel<T><<<dim3(cdiv(g.co, 128), bsplits), 128, 0, st>>>(dy, Mo, g.co, mchunk, bpart);
+      conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(net->ws, splits, g.co, K, g.c, g.k * g.k, l.W, l.VW,
+                                                                   keep ? l.GW : nullptr, l.Wbf, l.Wtbf, lr, mu);
+      bias_sgd_kernel<<<cdiv(g.co, 256), 256, 0, st>>>(bpart, bsplits, g.co, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
+      CE_CHECK_LAUNCH();
+    } else {  // pool
+      if (l.need_dx) {
+        ConvGeom g = l.g;
+        g.n = n;
+        size_t total = (size_t)n * g.h * g.w * g.c;
+        maxpool_bwd_kernel<T, T><<<grid_for(total), 256, 0, st>>>((const T*)gin, l.arg, g, mask, (T*)gout);
+        CE_CHECK_LAUNCH();
+      }
+    }
+    if (!l.need_dx) break;  // nothing below needs gradients
+    cur ^= 1;
+  }
+  return CE_OK;
+}
+
+template <class T>
+int enqueue_step(ce_net* net, int n, float lr, float mu) {
+  int s = enqueue_forward<T>(net, n);
+  if (s != CE_OK) return s;
+  const Layer& last = net->L.back();
+  xent_kernel<<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes, (float*)net->gbuf[0],
+                                        net->d_losses, net->d_step);
+  CE_CHECK_LAUNCH();
+  return enqueue_backward<T>(net, n, lr, mu);
+}
+
+int forward_any(ce_net* net, int n) {
+  return net->prec == CE_PREC_FP32 ? enqueue_forward<float>(net, n) : enqueue_forward<bf16>(net, n);
+}
+int step_any(ce_net* net, int n, float lr, float mu) {
+  return net->prec == CE_PREC_FP32 ? enqueue_step<float>(net, n, lr, mu) : enqueue_step<bf16>(net, n, lr, mu);
+}
+
+int gather_any(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm, int spe, int base, int B,
+               bool labels) {
+  dim3 grid(cdiv(ds->h * ds->w, 256), B);
+  int HW = ds->h * ds->w;
+  if (net->prec == CE_PREC_FP32)
+    gather_u8_kernel<float><<<grid, 256, 0, net->st>>>(ds->pix, ds->lab, perm, net->d_step, n_perm, spe, base, B,
+                                                       ds->c, net->in_cp, HW, (float*)net->x0,
+                                                       labels ? net->ybatch : nullptr);
+  else
+    gather_u8_kernel<bf16><<<grid, 256, 0, net->st>>>(ds->pix, ds->lab, perm, net->d_step, n_perm, spe, base, B,
+                                                      ds->c, net->in_cp, HW, (bf16*)net->x0,
+                                                      labels ? net->ybatch : nullptr);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+int upload_host_batch(ce_net* net, const float* x, int n) {
+  size_t elems = (size_t)n * net->in_c * net->in_h * net->in_w;
+  if (elems > net->xhost_cap) {
+    if (net->d_xhost) {
+      cudaFreeAsync(net->d_xhost, net->st);
+      net->allocs.erase(std::find(net->allocs.begin(), net->allocs.end(), (void*)net->d_xhost));
+    }
+    ALLOC(net->d_xhost, elems * 4);
+    net->xhost_cap = elems;
+  }
+  CE_CUDA(cudaMemcpyAsync(net->d_xhost, x, elems * 4, cudaMemcpyHostToDevice, net->st));
+  int HW = net->in_h * net->in_w;
+  size_t total = (size_t)n * HW;
+  if (net->prec == CE_PREC_FP32)
+    nchw_to_nhwc_kernel<float><<<grid_for(total), 256, 0, net->st>>>(net->d_xhost, n, net->in_c, net->in_cp, HW,
+                                                                      (float*)net->x0);
+  else
+    nchw_to_nhwc_kernel<bf16><<<grid_for(total), 256, 0, net->st>>>(net->d_xhost, n, net->in_c, net->in_cp, HW,
+                                                                     (bf16*)net->x0);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+int check_net(const ce_net* net) {
+  if (!net) return fail(CE_EINVAL, "null net");
+  return CE_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+int ce_version(void) { return 1; }
+const char* ce_last_error(void) { return g_err; }
+
+int ce_device_count(int* count) {
+  CE_CUDA(cudaGetDeviceCount(count));
+  return CE_OK;
+}
+
+int ce_dataset_create(int device, const uint8_t* pixels, const uint8_t* labels, int n, int c, int h, int w,
+                      ce_dataset** out) {
+  if (!pixels || !labels || !out || n <= 0 || c <= 0 || h <= 0 || w <= 0)
+    return fail(CE_EINVAL, "ce_dataset_create: bad arguments");
+  DevGuard dg(device);
+  ce_dataset* ds = new ce_dataset();
+  ds->device = device;
+  ds->n = n;
+  ds->c = c;
+  ds->h = h;
+  ds->w = w;
+  size_t bytes = (size_t)n * c * h * w;
+  cudaError_t e1 = cudaMalloc(&ds->pix, bytes);
+  cudaError_t e2 = cudaMalloc(&ds->lab, n);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaGetLastError();
+    if (ds->pix) cudaFree(ds->pix);
+    if (ds->lab) cudaFree(ds->lab);
+    delete ds;
+    return fail(CE_ENOMEM, "dataset allocation of %zu bytes failed", bytes);
+  }
+  CE_CUDA(cudaMemcpy(ds->pix, pixels, bytes, cudaMemcpyHostToDevice));
+  CE_CUDA(cudaMemcpy(ds->lab, labels, n, cudaMemcpyHostToDevice));
+  *out = ds;
+  return CE_OK;
+}
+
+int ce_dataset_destroy(ce_dataset* ds) {
+  if (!ds) return CE_OK;
+  DevGuard dg(ds->device);
+  cudaFree(ds->pix);
+  cudaFree(ds->lab);
+  delete ds;
+  return CE_OK;
+}
+
+int ce_net_destroy(ce_net* net) {
+  if (!net) return CE_OK;
+  DevGuard dg(net->device);
+  cudaStreamSynchronize(net->st);
+  for (void* p : net->allocs) cudaFreeAsync(p, net->st);
+  cudaStreamSynchronize(net->st);
+  cudaStreamDestroy(net->st);
+  delete net;
+  return CE_OK;
+}
+
+int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out) {
+  if (!d || !out || d->n_layers < 1 || !d->layers) return fail(CE_EINVAL, "ce_net_create: bad descriptor");
+  if (precision != CE_PREC_BF16 && precision != CE_PREC_FP32) return fail(CE_EINVAL, "bad precision %d", precision);
+  if (d->max_batch < 1 || d->max_batch > 1024) return fail(CE_EINVAL, "max_batch %d out of range", d->max_batch);
+  DevGuard dg(device);
+  ce_net* net = new ce_net();
+  net->device = device;
+  net->prec = precision;
+  net->in_c = d->in_c;
+  net->in_cp = (d->in_c + 7) / 8 * 8;
+  net->in_h = d->in_h;
+  net->in_w = d->in_w;
+  net->max_batch = d->max_batch;
+  cudaDeviceGetAttribute(&net->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&net->st, cudaStreamNonBlocking) != cudaSuccess) {
+    delete net;
+    return fail(CE_ECUDA, "stream creation failed");
+  }
+  net->use_tc = precision == CE_PREC_BF16 && conv_tc_enabled();
+  int rc = CE_OK;
+  auto bail = [&](int s) {
+    ce_net_destroy(net);
+    return s;
+  };
+  // ---- shapes
+  int c = d->in_c, cs = net->in_cp, h = d->in_h, w = d->in_w;
+  bool features_done = false, seen_param = false;
+  int prev_kind = 0, prev_relu = 0;
+  int units = 0;
+  for (int i = 0; i < d->n_layers; ++i) {
+    const ce_layer_desc& ld = d->layers[i];
+    Layer l;
+    l.kind = ld.kind;
+    if (ld.kind == CE_LAYER_CONV || ld.kind == CE_LAYER_POOL) {
+      if (features_done) return bail(fail(CE_EINVAL, "layer %d: feature layer after dense", i));
+      int k = ld.kernel, s = ld.stride;
+      if (k < 1 || s < 1) return bail(fail(CE_EINVAL, "layer %d: kernel and stride must be >= 1", i));
+      if (h < k || w < k) return bail(fail(CE_EINVAL, "layer %d: window %d exceeds input %dx%d", i, k, h, w));
+      l.g.c = cs;
+      l.g.h = h;
+      l.g.w = w;
+      l.g.k = k;
+      l.g.s = s;
+      l.g.oh = (h - k) / s + 1;
+      l.g.ow = (w - k) / s + 1;
+      l.c_real = c;
+      if (ld.kind == CE_LAYER_CONV) {
+        if (ld.out_channels < 1 || ld.out_channels % 8) return bail(fail(CE_EINVAL, "layer %d: out_channels %d not a multiple of 8", i, ld.out_channels));
+        l.g.co = ld.out_channels;
+        l.relu = ld.relu;
+        l.out_c_store = l.out_c_real = ld.out_channels;
+      } else {
+        l.g.co = cs;
+        l.out_c_store = cs;
+        l.out_c_real = c;
+      }
+      l.need_dx = seen_param;
+      l.mask_in = prev_kind == CE_LAYER_CONV && prev_relu;
+      l.out_per_sample = (size_t)l.g.oh * l.g.ow * l.out_c_store;
+      if (ld.kind == CE_LAYER_CONV) {
+        seen_param = true;
+        c = cs = l.g.co;
+      }
+      h = l.g.oh;
+      w = l.g.ow;
+    } else if (ld.kind == CE_LAYER_DENSE) {
+      if (ld.units < 1) return bail(fail(CE_EINVAL, "layer %d: dense units must be >= 1", i));
+      if (!features_done) {
+        l.in_units = h * w * cs;
+        l.hw_in = h * w;
+        l.c_real = c;
+        l.in_is_act = true;
+        features_done = true;
+      } else {
+        l.in_units = units;
+        l.hw_in = 0;
+        l.c_real = units;
+        l.in_is_act = false;
+      }
+      l.out_units = ld.units;
+      l.need_dx = seen_param;
+      l.mask_in = prev_kind == CE_LAYER_CONV && prev_relu;
+      l.out_per_sample = ld.units;
+      seen_param = true;
+      units = ld.units;
+    } else {
+      return bail(fail(CE_EINVAL, "layer %d: unknown kind %d", i, ld.kind));
+    }
+    prev_kind = ld.kind;
+    prev_relu = ld.relu;
+    net->L.push_back(l);
+  }
+  if (net->L.back().kind != CE_LAYER_DENSE) return bail(fail(CE_EINVAL, "network must end in a Dense layer"));
+  net->classes = net->L.back().out_units;
+  // ---- allocations
+  const size_t B = d->max_batch, ab = act_bytes(net);
+  size_t total_params = 0;
+  for (auto& l : net->L) {
+    if (l.kind == CE_LAYER_CONV) total_params += (size_t)l.g.co * l.g.k * l.g.k * l.g.c;
+    if (l.kind == CE_LAYER_DENSE) total_params += (size_t)l.out_units * l.in_units;
+  }
+  net->keep_grads = total_params <= (64u << 20);
+  size_t max_g = (size_t)B * net->in_cp * net->in_h * net->in_w * ab, ws = 0;
+  for (size_t i = 0; i < net->L.size(); ++i) {
+    Layer& l = net->L[i];
+    if (l.kind == CE_LAYER_DENSE) {
+      ALLOC(l.out, B * l.out_units * 4);
+      max_g = std::max(max_g, B * l.out_units * 4);
+      max_g = std::max(max_g, B * (size_t)l.in_units * (l.in_is_act ? ab : 4));
+      l.wn = (size_t)l.out_units * l.in_units;
+      l.bn = l.out_units;
+      long long bps = (long long)cdiv(B, SG_BM) * cdiv(l.out_units, SG_BN);
+      int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms));
+      ws = std::max(ws, (size_t)sp * B * l.out_units * 4);
+      ws = std::max(ws, (size_t)l.out_units * 4);
+    } else {
+      ALLOC(l.out, B * l.out_per_sample * ab);
+      max_g = std::max(max_g, B * l.out_per_sample * ab);
+      if (l.kind == CE_LAYER_POOL) ALLOC(l.arg, B * l.out_per_sample);
+      if (l.kind == CE_LAYER_CONV) {
+        const int K = l.g.k * l.g.k * l.g.c;
+        l.wn = (size_t)l.g.co * K;
+        l.bn = l.g.co;
+        long long Mo = (long long)B * l.g.oh * l.g.ow;
+        long long bps = (long long)cdiv(l.g.co, SG_BM) * cdiv(K, SG_BN);
+        int sp = simt_splits((int)Mo, pick_splits(bps, Mo, 512, net->num_sms));
+        sp = std::max(sp, conv_wgrad_tc_max_splits(l.g, (int)B, net->num_sms));
+        ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)64 * l.g.co * 4);
+      }
+    }
+    if (l.wn) {
+      l.pidx = (int)net->params.size();
+      net->params.push_back((int)i);
+      ALLOC(l.W, l.wn * 4);
+      ALLOC(l.VW, l.wn * 4);
+      ALLOC(l.b, l.bn * 4);
+      ALLOC(l.Vb, l.bn * 4);
+      if (net->keep_grads) {
+        ALLOC(l.GW, l.wn * 4);
+        ALLOC(l.Gb, l.bn * 4);
+      }
+      if (precision == CE_PREC_BF16 && l.kind == CE_LAYER_CONV) {
+        ALLOC(l.Wbf, l.wn * 2);
+        ALLOC(l.Wtbf, l.wn * 2);
+      }
+      cudaMemsetAsync(l.W, 0, l.wn * 4, net->st);
+      cudaMemsetAsync(l.VW, 0, l.wn * 4, net->st);
+      cudaMemsetAsync(l.b, 0, l.bn * 4, net->st);
+      cudaMemsetAsync(l.Vb, 0, l.bn * 4, net->st);
+    }
+  }
+  ALLOC(net->x0, B * net->in_cp * net->in_h * net->in_w * ab);
+  ALLOC(net->ybatch, B * 4);
+  ALLOC(net->gbuf[0], max_g);
+  ALLOC(net->gbuf[1], max_g);
+  net->gbytes = max_g;
+  ALLOC(net->ws, ws);
+  net->ws_bytes = ws;
+  ALLOC(net->d_step, 16);
+  net->losses_cap = 4096;
+  ALLOC(net->d_losses, net->losses_cap * 4);
+  cudaError_t e = cudaStreamSynchronize(net->st);
+  if (e != cudaSuccess) return bail(fail(CE_ECUDA, "net create: %s", cudaGetErrorString(e)));
+  (void)rc;
+  *out = net;
+  return CE_OK;
+}
+
+int ce_net_device_bytes(const ce_net* net, size_t* bytes) {
+  if (check_net(net)) return CE_EINVAL;
+  *bytes = net->bytes;
+  return CE_OK;
+}
+
+int ce_net_num_param_layers(const ce_net* net, int* count) {
+  if (check_net(net)) return CE_EINVAL;
+  *count = (int)net->params.size();
+  return CE_OK;
+}
+
+static int param_layer(ce_net* net, int p, Layer** out) {
+  if (!net || p < 0 || p >= (int)net->params.size()) return fail(CE_EINVAL, "param layer %d out of range", p);
+  *out = &net->L[net->params[p]];
+  return CE_OK;
+}
+
+static size_t host_w_count(const Layer& l) {
+  if (l.kind == CE_LAYER_CONV) return (size_t)l.g.co * l.c_real * l.g.k * l.g.k;
+  if (l.in_is_act) return (size_t)l.out_units * l.hw_in * l.c_real;
+  return (size_t)l.out_units * l.in_units;
+}
+
+int ce_net_set_params(ce_net* net, int p, const float* w, const float* b) {
+  Layer* lp;
+  if (int s = param_layer(net, p, &lp)) return s;
+  Layer& l = *lp;
+  DevGuard dg(net->device);
+  cudaStream_t st = net->st;
+  size_t hn = host_w_count(l);
+  // stage through a temporary in chunks of rows to bound memory for giant heads
+  size_t rows = l.kind == CE_LAYER_CONV ? (size_t)l.g.co : (size_t)l.out_units;
+  size_t hrow = hn / rows, drow = l.wn / rows;
+  size_t chunk_rows = std::max<size_t>(1, std::min(rows, (size_t)(256u << 20) / (hrow * 4)));
+  float* tmp = nullptr;
+  CE_CUDA(cudaMallocAsync(&tmp, chunk_rows * hrow * 4, st));
+  for (size_t r0 = 0; r0 < rows; r0 += chunk_rows) {
+    size_t nr = std::min(chunk_rows, rows - r0);
+    CE_CUDA(cudaMemcpyAsync(tmp, w + r0 * hrow, nr * hrow * 4, cudaMemcpyHostToDevice, st));
+    float* dst = l.W + r0 * drow;
+    if (l.kind == CE_LAYER_CONV)
+      conv_w_to_dev_kernel<<<grid_for(nr * drow), 256, 0, st>>>(tmp, (int)nr, l.c_real, l.g.c, l.g.k, dst);
+    else if (l.in_is_act)
+      dense_w_to_dev_kernel<<<grid_for(nr * drow), 256, 0, st>>>(tmp, nr, l.c_real, l.in_units / l.hw_in, l.hw_in,
+                                                                   dst);
+    else
+      CE_CUDA(cudaMemcpyAsync(dst, tmp, nr * drow * 4, cudaMemcpyDeviceToDevice, st));
+    CE_CHECK_LAUNCH();
+  }
+  CE_CUDA(cudaFreeAsync(tmp, st));
+  if (b) CE_CUDA(cudaMemcpyAsync(l.b, b, l.bn * 4, cudaMemcpyHostToDevice, st));
+  else CE_CUDA(cudaMemsetAsync(l.b, 0, l.bn * 4, st));
+  CE_CUDA(cudaMemsetAsync(l.VW, 0, l.wn * 4, st));
+  CE_CUDA(cudaMemsetAsync(l.Vb, 0, l.bn * 4, st));
+  if (l.Wbf) f32_to_bf16_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.wn, l.Wbf);
+  if (l.Wtbf) conv_wt_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.g.co, l.g.k * l.g.k, l.g.c, l.Wtbf);
+  CE_CHECK_LAUNCH();
+  CE_CUDA(cudaStreamSynchronize(st));
+  return CE_OK;
+}
+
+static int download_w(ce_net* net, const Layer& l, const float* dsrc, float* hdst) {
+  cudaStream_t st = net->st;
+  size_t hn = host_w_count(l);
+  if (l.kind == CE_LAYER_DENSE && !l.in_is_act) {
+    CE_CUDA(cudaMemcpyAsync(hdst, dsrc, hn * 4, cudaMemcpyDeviceToHost, st));
+    return CE_OK;
+  }
+  float* tmp = nullptr;
+  CE_CUDA(cudaMallocAsync(&tmp, hn * 4, st));
+  if (l.kind == CE_LAYER_CONV)
+    conv_w_to_host_kernel<<<grid_for(hn), 256, 0, st>>>(dsrc, l.g.co, l.c_real, l.g.c, l.g.k, tmp);
+  else
+    dense_w_to_host_kernel<<<grid_for(hn), 256, 0, st>>>(dsrc, l.out_units, l.c_real, l.in_units / l.hw_in, l.hw_in,
+                                                          tmp);
+  CE_CHECK_LAUNCH();
+  CE_CUDA(cudaMemcpyAsync(hdst, tmp, hn * 4, cudaMemcpyDeviceToHost, st));
+  CE_CUDA(cudaFreeAsync(tmp, st));
+  return CE_OK;
+}
+
+int ce_net_get_params(ce_net* net, int p, float* w, float* b, float* vw, float* vb) {
+  Layer* lp;
+  if (int s = param_layer(net, p, &lp)) return s;
+  DevGuard dg(net->device);
+  if (w) if (int s = download_w(net, *lp, lp->W, w)) return s;
+  if (vw) if (int s = download_w(net, *lp, lp->VW, vw)) return s;
+  if (b) CE_CUDA(cudaMemcpyAsync(b, lp->b, lp->bn * 4, cudaMemcpyDeviceToHost, net->st));
+  if (vb) CE_CUDA(cudaMemcpyAsync(vb, lp->Vb, lp->bn * 4, cudaMemcpyDeviceToHost, net->st));
+  CE_CUDA(cudaStreamSynchronize(net->st));
+  return CE_OK;
+}
+
+int ce_net_get_grads(ce_net* net, int p, float* gw, float* gb) {
+  Layer* lp;
+  if (int s = param_layer(net, p, &lp)) return s;
+  if (!lp->GW) return fail(CE_EINVAL, "gradients are not retained for nets above 64M parameters");
+  DevGuard dg(net->device);
+  if (gw) if (int s = download_w(net, *lp, lp->GW, gw)) return s;
+  if (gb) CE_CUDA(cudaMemcpyAsync(gb, lp->Gb, lp->bn * 4, cudaMemcpyDeviceToHost, net->st));
+  CE_CUDA(cudaStreamSynchronize(net->st));
+  return CE_OK;
+}
+
+int ce_net_forward_host(ce_net* net, const float* x, int n, float* logits) {
+  if (check_net(net)) return CE_EINVAL;
+  if (n < 1 || n > net->max_batch) return fail(CE_EINVAL, "batch %d outside [1, %d]", n, net->max_batch);
+  DevGuard dg(net->device);
+  if (int s = upload_host_batch(net, x, n)) return s;
+  if (int s = forward_any(net, n)) return s;
+  if (logits)
+    CE_CUDA(cudaMemcpyAsync(logits, net->L.back().out, (size_t)n * net->classes * 4, cudaMemcpyDeviceToHost, net->st));
+  CE_CUDA(cudaStreamSynchronize(net->st));
+  return CE_OK;
+}
+
+int ce_net_get_activation(ce_net* net, int layer, int n, float* out) {
+  if (check_net(net)) return CE_EINVAL;
+  if (layer < 0 || layer >= (int)net->L.size()) return fail(CE_EINVAL, "layer %d out of range", layer);
+  if (n < 1 || n > net->max_batch) return fail(CE_EINVAL, "bad n");
+  DevGuard dg(net->device);
+  Layer& l = net->L[layer];
+  cudaStream_t st = net->st;
+  if (l.kind == CE_LAYER_DENSE) {
+    CE_CUDA(cudaMemcpyAsync(out, l.out, (size_t)n * l.out_units * 4, cudaMemcpyDeviceToHost, st));
+  } else {
+    int HW = l.g.oh * l.g.ow;
+    size_t total = (size_t)n * l.out_c_real * HW;
+    float* tmp;
+    CE_CUDA(cudaMallocAsync(&tmp, total * 4, st));
+    if (net->prec == CE_PREC_FP32)
+      nhwc_to_nchw_kernel<float><<<grid_for(total), 256, 0, st>>>((const float*)l.out, n, l.out_c_real, l.out_c_store,
+                                                                  HW, tmp);
+    else
+      nhwc_to_nchw_kernel<bf16><<<grid_for(total), 256, 0, st>>>((const bf16*)l.out, n, l.out_c_real, l.out_c_store,
+                                                                 HW, tmp);
+    CE_CHECK_LAUNCH();
+    CE_CUDA(cudaMemcpyAsync(out, tmp, total * 4, cudaMemcpyDeviceToHost, st));
+    CE_CUDA(cudaFreeAsync(tmp, st));
+  }
+  CE_CUDA(cudaStreamSynchronize(st));
+  return CE_OK;
+}
+
+int ce_net_train_batch_host(ce_net* net, const float* x, const int64_t* labels, int n, float lr, float momentum,
+                            float* loss) {
+  if (check_net(net)) return CE_EINVAL;
+  if (n < 1 || n > net->max_batch) return fail(CE_EINVAL, "batch %d outside [1, %d]", n, net->max_batch);
+  DevGuard dg(net->device);
+  std::vector<int32_t> y(n);
+  for (int i = 0; i < n; ++i) {
+    if (labels[i] < 0 || labels[i] >= net->classes) return fail(CE_EINVAL, "labels must lie in [0, %d]", net->classes - 1);
+    y[i] = (int32_t)labels[i];
+  }
+  if (int s = upload_host_batch(net, x, n)) return s;
+  CE_CUDA(cudaMemcpyAsync(net->ybatch, y.data(), n * 4, cudaMemcpyHostToDevice, net->st));
+  CE_CUDA(cudaMemsetAsync(net->d_step, 0, 4, net->st));
+  if (int s = step_any(net, n, lr, momentum)) return s;
+  CE_CUDA(cudaMemcpyAsync(loss, net->d_losses, 4, cudaMemcpyDeviceToHost, net->st));
+  CE_CUDA(cudaStreamSynchronize(net->st));
+  return CE_OK;
+}
+
+int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm, int epochs, int steps_per_epoch,
+               int batch, float lr, float momentum, float* losses, double* device_ms) {
+  if (check_net(net)) return CE_EINVAL;
+  if (!ds || !perm || epochs < 1 || steps_per_epoch < 1 || batch < 1 || batch > net->max_batch)
+    return fail(CE_EINVAL, "ce_train: bad arguments");
+  if (ds->c != net->in_c || ds->h != net->in_h || ds->w != net->in_w)
+    return fail(CE_EINVAL, "dataset shape does not match the network input");
+  if ((long long)steps_per_epoch * batch > n_perm) return fail(CE_EINVAL, "steps_per_epoch * batch exceeds n");
+  DevGuard dg(net->device);
+  cudaStream_t st = net->st;
+  const int steps = epochs * steps_per_epoch;
+  if (steps > net->losses_cap) {
+    ALLOC(net->d_losses, (size_t)steps * 4);
+    net->losses_cap = steps;
+  }
+  size_t pn = (size_t)epochs * n_perm;
+  if (pn > net->perm_cap) {
+    ALLOC(net->d_perm, pn * 4);
+    net->perm_cap = pn;
+  }
+  CE_CUDA(cudaMemcpyAsync(net->d_perm, perm, pn * 4, cudaMemcpyHostToDevice, st));
+  CE_CUDA(cudaMemsetAsync(net->d_step, 0, 4, st));
+  // capture one step
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool graphed = false;
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true);
+    if (s == CE_OK) s = step_any(net, batch, lr, momentum);
+    cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (s != CE_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return s;
+    }
+    if (ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) graphed = true;
+    if (graph) cudaGraphDestroy(graph);
+  }
+  cudaGetLastError();
+  cudaEvent_t e0, e1;
+  CE_CUDA(cudaEventCreate(&e0));
+  CE_CUDA(cudaEventCreate(&e1));
+  CE_CUDA(cudaEventRecord(e0, st));
+  for (int i = 0; i < steps; ++i) {
+    if (graphed) {
+      CE_CUDA(cudaGraphLaunch(exec, st));
+    } else {
+      if (int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true)) return s;
+      if (int s = step_any(net, batch, lr, momentum)) return s;
+    }
+  }
+  CE_CUDA(cudaEventRecord(e1, st));
+  CE_CUDA(cudaMemcpyAsync(losses, net->d_losses, (size_t)steps * 4, cudaMemcpyDeviceToHost, st));
+  cudaError_t se = cudaStreamSynchronize(st);
+  if (exec) cudaGraphExecDestroy(exec);
+  if (se != cudaSuccess) return fail(CE_ECUDA, "train loop: %s", cudaGetErrorString(se));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (device_ms) *device_ms = ms;
+  return CE_OK;
+}
+
+int ce_predict(ce_net* net, const ce_dataset* ds, int batch, double* scores, int64_t* preds) {
+  if (check_net(net)) return CE_EINVAL;
+  if (!ds || batch < 1 || batch > net->max_batch) return fail(CE_EINVAL, "ce_predict: bad arguments");
+  DevGuard dg(net->device);
+  cudaStream_t st = net->st;
+  if ((size_t)ds->n > net->pred_cap) {
+    ALLOC(net->d_scores, (size_t)ds->n * 8);
+    ALLOC(net->d_preds, (size_t)ds->n * 8);
+    net->pred_cap = ds->n;
+  }
+  for (int start = 0; start < ds->n; start += batch) {
+    int nb = std::min(batch, ds->n - start);
+    if (int s = gather_any(net, ds, nullptr, 0, 1, start, nb, false)) return s;
+    if (int s = forward_any(net, nb)) return s;
+    predict_head_kernel<<<cdiv(nb, 128), 128, 0, st>>>((const float*)net->L.back().out, nb, net->classes, start,
+                                                        net->d_scores, net->d_preds);
+    CE_CHECK_LAUNCH();
+  }
+  CE_CUDA(cudaMemcpyAsync(scores, net->d_scores, (size_t)ds->n * 8, cudaMemcpyDeviceToHost, st));
+  CE_CUDA(cudaMemcpyAsync(preds, net->d_preds, (size_t)ds->n * 8, cudaMemcpyDeviceToHost, st));
+  CE_CUDA(cudaStreamSynchronize(st));
+  return CE_OK;
+}
+
+int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double* seconds) {
+  if (check_net(net)) return CE_EINVAL;
+  if (n < 1 || n > net->max_batch || warmup < 0 || reps < 1) return fail(CE_EINVAL, "ce_latency: bad arguments");
+  DevGuard dg(net->device);
+  cudaStream_t st = net->st;
+  if (int s = upload_host_batch(net, x, n)) return s;
+  for (int i = 0; i < warmup; ++i)
+    if (int s = forward_any(net, n)) return s;
+  std::vector<cudaEvent_t> ev(2 * reps);
+  for (auto& e : ev) CE_CUDA(cudaEventCreate(&e));
+  for (int r = 0; r < reps; ++r) {
+    CE_CUDA(cudaEventRecord(ev[2 * r], st));
+    if (int s = forward_any(net, n)) return s;
+    CE_CUDA(cudaEventRecord(ev[2 * r + 1], st));
+  }
+  CE_CUDA(cudaStreamSynchronize(st));
+  for (int r = 0; r < reps; ++r) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[2 * r], ev[2 * r + 1]);
+    seconds[r] = ms * 1e-3;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return CE_OK;
+}
+
+}  // extern "C"

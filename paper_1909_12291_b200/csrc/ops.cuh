@@ -1,0 +1,307 @@
+// Element-wise / reduction kernels of the training step: batch gather and
+// normalisation, max-pool forward/backward, column sums, fused SGD updates,
+// dense split-K reduction, softmax cross-entropy, prediction head and the
+// host-layout <-> device-layout parameter permutations.
+#pragma once
+#include "kernels.cuh"
+
+namespace ce {
+
+// ---------------------------------------------------------------- input
+// x[b][y][x][cp] = cp < C ? pix[idx[b]][cp][y][x] / 255 : 0      (data.py:65-66)
+// idx source: perm[epoch*n_perm + bi*B + b] with (epoch, bi) from the device
+// step counter (graph-replayable), or a plain base index (predict).
+template <class T>
+__global__ void gather_u8_kernel(const uint8_t* __restrict__ pix, const uint8_t* __restrict__ labels,
+                                 const int32_t* __restrict__ perm, const int* __restrict__ step_ctr, int n_perm,
+                                 int steps_per_epoch, int base, int B, int C, int Cp, int HW, T* __restrict__ x,
+                                 int32_t* __restrict__ y) {
+  const int b = blockIdx.y;
+  int src;
+  if (perm) {
+    const int step = *step_ctr;
+    const int epoch = step / steps_per_epoch, bi = step - epoch * steps_per_epoch;
+    src = perm[(size_t)epoch * n_perm + (size_t)bi * B + b];
+  } else {
+    src = base + b;
+  }
+  const uint8_t* img = pix + (size_t)src * C * HW;
+  for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < HW; px += gridDim.x * blockDim.x) {
+    T* dst = x + ((size_t)b * HW + px) * Cp;
+    for (int c = 0; c < Cp; ++c) {
+      float v = c < C ? __fdiv_rn((float)img[(size_t)c * HW + px], 255.0f) : 0.f;
+      stf(dst, c, v);
+    }
+  }
+  if (y && blockIdx.x == 0 && threadIdx.x == 0) y[b] = labels[src];
+}
+
+// fp32 NCHW (host batch) -> T NHWC padded
+template <class T>
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ in, int B, int C, int Cp, int HW, T* __restrict__ x) {
+  size_t total = (size_t)B * HW;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t b = e / HW, px = e % HW;
+    for (int c = 0; c < Cp; ++c) stf(x + e * Cp, c, c < C ? in[(b * C + c) * HW + px] : 0.f);
+  }
+}
+
+// T NHWC (Cp) -> fp32 NCHW (C)
+template <class T>
+__global__ void nhwc_to_nchw_kernel(const T* __restrict__ x, int B, int C, int Cp, int HW, float* __restrict__ out) {
+  size_t total = (size_t)B * C * HW;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t px = e % HW, t = e / HW;
+    size_t c = t % C, b = t / C;
+    out[e] = ldf(x, (b * HW + px) * Cp + c);
+  }
+}
+
+// ---------------------------------------------------------------- max pool
+// ties -> first window element in row-major order (nn.py:119-150)
+template <class T>
+__global__ void maxpool_fwd_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y, uint8_t* __restrict__ arg) {
+  size_t total = (size_t)g.n * g.oh * g.ow * g.c;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int c = e % g.c;
+    size_t t = e / g.c;
+    int q = t % g.ow;
+    t /= g.ow;
+    int p = t % g.oh;
+    int n = t / g.oh;
+    const T* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c + c;
+    float best = ldf(base, 0);
+    int bi = 0;
+    for (int i = 0; i < g.k; ++i)
+      for (int j = 0; j < g.k; ++j) {
+        float v = ldf(base, ((size_t)i * g.w + j) * g.c);
+        if (v > best) {
+          best = v;
+          bi = i * g.k + j;
+        }
+      }
+    stf(y, e, best);
+    if (arg) arg[e] = (uint8_t)bi;
+  }
+}
+
+// gather form: dx[n,h,w,c] = sum over windows (p,q) whose argmax hits (h,w)
+template <class T, class TG>
+__global__ void maxpool_bwd_kernel(const TG* __restrict__ dy, const uint8_t* __restrict__ arg, ConvGeom g,
+                                   const T* __restrict__ mask, TG* __restrict__ dx) {
+  size_t total = (size_t)g.n * g.h * g.w * g.c;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int c = e % g.c;
+    size_t t = e / g.c;
+    int wx = t % g.w;
+    t /= g.w;
+    int hy = t % g.h;
+    int n = t / g.h;
+    float acc = 0.f;
+    int p_lo = hy - g.k + 1 > 0 ? (hy - g.k + 1 + g.s - 1) / g.s : 0;
+    int p_hi = min(hy / g.s, g.oh - 1);
+    int q_lo = wx - g.k + 1 > 0 ? (wx - g.k + 1 + g.s - 1) / g.s : 0;
+    int q_hi = min(wx / g.s, g.ow - 1);
+    for (int p = p_lo; p <= p_hi; ++p)
+      for (int q = q_lo; q <= q_hi; ++q) {
+        size_t o = (((size_t)n * g.oh + p) * g.ow + q) * g.c + c;
+        int hit = (hy - p * g.s) * g.k + (wx - q * g.s);
+        if (arg[o] == hit) acc += ldf(dy, o);
+      }
+    if (mask && !(ldf(mask, e) > 0.f)) acc = 0.f;
+    stf(dx, e, acc);
+  }
+}
+
+// ---------------------------------------------------------------- reductions
+// part[split][o] = sum_{m in split} dy[m][o]
+template <class T>
+__global__ void colsum_partial_kernel(const T* __restrict__ dy, int M, int N, int mchunk, float* __restrict__ part) {
+  const int split = blockIdx.y;
+  const int m0 = split * mchunk, m1 = min(M, m0 + mchunk);
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < N; o += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int m = m0; m < m1; ++m) acc += ldf(dy, (size_t)m * N + o);
+    part[(size_t)split * N + o] = acc;
+  }
+}
+
+// conv weights: g = sum_split part[split][o][kk]; momentum update of W (fp32 master)
+// plus bf16 mirrors W[o][kk] and Wt[c][tap][o] (dgrad operand of the tensor path)
+__global__ void conv_sgd_kernel(const float* __restrict__ part, int splits, int co, int K, int cp, int taps,
+                                float* __restrict__ w, float* __restrict__ vel, float* __restrict__ gw,
+                                bf16* __restrict__ wbf, bf16* __restrict__ wtbf, float lr, float mu) {
+  size_t total = (size_t)co * K;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    float g = 0.f;
+    for (int s = 0; s < splits; ++s) g += part[(size_t)s * total + e];
+    if (gw) gw[e] = g;
+    float wv = w[e], vv = vel[e];
+    sgd_update(wv, vv, g, lr, mu);
+    w[e] = wv;
+    vel[e] = vv;
+    if (wbf) wbf[e] = __float2bfloat16_rn(wv);
+    if (wtbf) {
+      int o = e / K, kk = e % K;
+      int c = kk % cp, tap = kk / cp;
+      wtbf[((size_t)c * taps + tap) * co + o] = __float2bfloat16_rn(wv);
+    }
+  }
+}
+
+// bias: g = sum_split part[split][o]
+__global__ void bias_sgd_kernel(const float* __restrict__ part, int splits, int n, float* __restrict__ b,
+                                float* __restrict__ vel, float* __restrict__ gb, float lr, float mu) {
+  int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  float g = 0.f;
+  for (int s = 0; s < splits; ++s) g += part[(size_t)s * n + o];
+  if (gb) gb[o] = g;
+  float bv = b[o], vv = vel[o];
+  sgd_update(bv, vv, g, lr, mu);
+  b[o] = bv;
+  vel[o] = vv;
+}
+
+// dense forward reduce: y[b][o] = bias[o] + sum_split part[split][b][o]
+__global__ void dense_reduce_kernel(const float* __restrict__ part, int splits, int B, int out,
+                                    const float* __restrict__ bias, float* __restrict__ y) {
+  size_t total = (size_t)B * out;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += part[(size_t)s * total + e];
+    y[e] = acc + bias[e % out];
+  }
+}
+
+// ---------------------------------------------------------------- loss
+// softmax cross-entropy (nn.py:287-303), one block, B <= 1024:
+// loss = -mean(logp[label]); grad = (softmax - onehot) / B.
+// Writes losses[*step] and advances the step counter (end of the step).
+__global__ void xent_kernel(const float* __restrict__ logits, const int32_t* __restrict__ y, int B, int K,
+                            float* __restrict__ grad, float* __restrict__ losses, int* __restrict__ step_ctr) {
+  __shared__ double red[1024];
+  const int b = threadIdx.x;
+  double lp = 0.0;
+  if (b < B) {
+    const float* z = logits + (size_t)b * K;
+    float mx = z[0];
+    for (int k = 1; k < K; ++k) mx = fmaxf(mx, z[k]);
+    float se = 0.f;
+    for (int k = 0; k < K; ++k) se += expf(z[k] - mx);
+    float lse = logf(se);
+    const int lab = y[b];
+    for (int k = 0; k < K; ++k) {
+      float logp = (z[k] - mx) - lse;
+      float gk = expf(logp);
+      if (k == lab) {
+        gk -= 1.0f;
+        lp = (double)logp;
+      }
+      grad[(size_t)b * K + k] = gk / (float)B;
+    }
+  }
+  red[threadIdx.x] = lp;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int step = *step_ctr;
+    losses[step] = (float)(-red[0] / B);
+    *step_ctr = step + 1;
+  }
+}
+
+// predict head (evaluator.py:179-185): p = softmax(logits); score = p[:,1]; pred = argmax
+__global__ void predict_head_kernel(const float* __restrict__ logits, int B, int K, int base,
+                                    double* __restrict__ scores, int64_t* __restrict__ preds) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const float* z = logits + (size_t)b * K;
+  float mx = z[0];
+  int am = 0;
+  for (int k = 1; k < K; ++k)
+    if (z[k] > mx) {
+      mx = z[k];
+      am = k;
+    }
+  float se = 0.f;
+  for (int k = 0; k < K; ++k) se += expf(z[k] - mx);
+  scores[base + b] = (double)(expf(z[1] - mx) / se);
+  preds[base + b] = am;
+}
+
+// ---------------------------------------------------------------- parameter layouts
+// conv: host (o, c, i, j) <-> device [o][i][j][cp]
+__global__ void conv_w_to_dev_kernel(const float* __restrict__ hw, int co, int c, int cp, int k, float* __restrict__ w) {
+  size_t total = (size_t)co * k * k * cp;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int ch = e % cp;
+    size_t t = e / cp;
+    int j = t % k;
+    t /= k;
+    int i = t % k;
+    int o = t / k;
+    w[e] = ch < c ? hw[(((size_t)o * c + ch) * k + i) * k + j] : 0.f;
+  }
+}
+__global__ void conv_w_to_host_kernel(const float* __restrict__ w, int co, int c, int cp, int k, float* __restrict__ hw) {
+  size_t total = (size_t)co * c * k * k;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int j = e % k;
+    size_t t = e / k;
+    int i = t % k;
+    t /= k;
+    int ch = t % c;
+    int o = t / c;
+    hw[e] = w[(((size_t)o * k + i) * k + j) * cp + ch];
+  }
+}
+// dense after features: host column (c, h, w) <-> device column (h, w, cp)
+__global__ void dense_w_to_dev_kernel(const float* __restrict__ hw, size_t rows, int c, int cp, int hwsz,
+                                      float* __restrict__ w) {
+  size_t in_dev = (size_t)hwsz * cp, in_host = (size_t)hwsz * c;
+  size_t total = rows * in_dev;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t r = e / in_dev, col = e % in_dev;
+    int ch = col % cp;
+    size_t px = col / cp;
+    w[e] = ch < c ? hw[r * in_host + (size_t)ch * hwsz + px] : 0.f;
+  }
+}
+__global__ void dense_w_to_host_kernel(const float* __restrict__ w, size_t rows, int c, int cp, int hwsz,
+                                       float* __restrict__ hw) {
+  size_t in_dev = (size_t)hwsz * cp, in_host = (size_t)hwsz * c;
+  size_t total = rows * in_host;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t r = e / in_host, col = e % in_host;
+    int ch = col / hwsz;
+    size_t px = col % hwsz;
+    hw[e] = w[r * in_dev + px * cp + ch];
+  }
+}
+__global__ void f32_to_bf16_kernel(const float* __restrict__ a, size_t n, bf16* __restrict__ b) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    b[e] = __float2bfloat16_rn(a[e]);
+}
+__global__ void conv_wt_kernel(const float* __restrict__ w, int co, int taps, int cp, bf16* __restrict__ wt) {
+  size_t total = (size_t)co * taps * cp;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int c = e % cp;
+    size_t t = e / cp;
+    int tap = t % taps;
+    int o = t / taps;
+    wt[((size_t)c * taps + tap) * co + o] = __float2bfloat16_rn(w[e]);
+  }
+}
+
+inline int grid_for(size_t n, int threads = 256) {
+  size_t g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace ce

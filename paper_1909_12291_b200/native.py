@@ -1,0 +1,222 @@
+"""ctypes binding of libmenndl_sm100.so (include/menndl_sm100.h).
+
+ctypes releases the GIL for the duration of each foreign call, so worker
+threads driving different nets (different GPUs / streams) run concurrently.
+There is no fallback: if the library is missing the import of this module
+fails loudly (build it with paper_1909_12291_b200.build).
+"""
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import build as _build
+from .faults import CE_OK, status_to_exception
+
+LAYER_CONV, LAYER_POOL, LAYER_DENSE = 1, 2, 3
+PREC_BF16, PREC_FP32 = 0, 1
+PRECISIONS = {"bf16": PREC_BF16, "fp32": PREC_FP32}
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [("kind", C.c_int), ("out_channels", C.c_int), ("kernel", C.c_int),
+                ("stride", C.c_int), ("relu", C.c_int), ("units", C.c_int)]
+
+
+class NetDesc(C.Structure):
+    _fields_ = [("in_c", C.c_int), ("in_h", C.c_int), ("in_w", C.c_int), ("n_layers", C.c_int),
+                ("layers", C.POINTER(LayerDesc)), ("max_batch", C.c_int)]
+
+
+_P = C.c_void_p
+_F = C.POINTER(C.c_float)
+_D = C.POINTER(C.c_double)
+_I32 = C.POINTER(C.c_int32)
+_I64 = C.POINTER(C.c_int64)
+_U8 = C.POINTER(C.c_uint8)
+
+_SIGNATURES = {
+    "ce_version": ([], C.c_int),
+    "ce_last_error": ([], C.c_char_p),
+    "ce_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "ce_dataset_create": ([C.c_int, _U8, _U8, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
+    "ce_dataset_destroy": ([_P], C.c_int),
+    "ce_net_create": ([C.POINTER(NetDesc), C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
+    "ce_net_destroy": ([_P], C.c_int),
+    "ce_net_device_bytes": ([_P, C.POINTER(C.c_size_t)], C.c_int),
+    "ce_net_num_param_layers": ([_P, C.POINTER(C.c_int)], C.c_int),
+    "ce_net_set_params": ([_P, C.c_int, _F, _F], C.c_int),
+    "ce_net_get_params": ([_P, C.c_int, _F, _F, _F, _F], C.c_int),
+    "ce_net_get_grads": ([_P, C.c_int, _F, _F], C.c_int),
+    "ce_net_forward_host": ([_P, _F, C.c_int, _F], C.c_int),
+    "ce_net_get_activation": ([_P, C.c_int, C.c_int, _F], C.c_int),
+    "ce_net_train_batch_host": ([_P, _F, _I64, C.c_int, C.c_float, C.c_float, _F], C.c_int),
+    "ce_train": ([_P, _P, _I32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float, _F, _D], C.c_int),
+    "ce_predict": ([_P, _P, C.c_int, _D, _I64], C.c_int),
+    "ce_latency": ([_P, _F, C.c_int, C.c_int, C.c_int, _D], C.c_int),
+}
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path():
+    return _build.LIB_PATH
+
+
+def load(build_if_missing=True):
+    """Load (building first if needed) and return the CDLL."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = library_path()
+        if not os.path.exists(path) or (build_if_missing and not _build.up_to_date()):
+            if not build_if_missing:
+                raise OSError(f"{path} missing; run python -m paper_1909_12291_b200.build")
+            _build.build()
+        lib = C.CDLL(path)
+        for name, (argtypes, restype) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes, fn.restype = argtypes, restype
+        _lib = lib
+        return lib
+
+
+def check(status):
+    if status != CE_OK:
+        msg = load().ce_last_error().decode(errors="replace")
+        raise status_to_exception(status, msg)
+
+
+def fptr(a):
+    return a.ctypes.data_as(_F) if a is not None else None
+
+
+def device_count():
+    n = C.c_int(0)
+    check(load().ce_device_count(C.byref(n)))
+    return n.value
+
+
+class Dataset:
+    """A PatchSet resident on one device (u8 pixels + labels)."""
+
+    def __init__(self, pset, device=0):
+        lib = load()
+        px = np.ascontiguousarray(pset.pixels, dtype=np.uint8)
+        lab = np.ascontiguousarray(pset.labels, dtype=np.uint8)
+        n, c, h, w = px.shape
+        self.n, self.shape, self.device = n, (c, h, w), device
+        self.labels = lab
+        h_ = _P()
+        check(lib.ce_dataset_create(device, px.ctypes.data_as(_U8), lab.ctypes.data_as(_U8), n, c, h, w,
+                                    C.byref(h_)))
+        self._h = h_
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            load().ce_dataset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Net:
+    """Owning wrapper of a ce_net handle."""
+
+    def __init__(self, layers, input_shape, max_batch, device=0, precision="bf16"):
+        lib = load()
+        arr = (LayerDesc * len(layers))()
+        for i, spec in enumerate(layers):
+            arr[i] = LayerDesc(*spec)
+        c, h, w = input_shape
+        desc = NetDesc(c, h, w, len(layers), arr, int(max_batch))
+        h_ = _P()
+        check(lib.ce_net_create(C.byref(desc), int(device), PRECISIONS[precision], C.byref(h_)))
+        self._h = h_
+        self.device, self.precision, self.max_batch = device, precision, max_batch
+
+    def close(self):
+        if self._h:
+            load().ce_net_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def device_bytes(self):
+        n = C.c_size_t(0)
+        check(load().ce_net_device_bytes(self._h, C.byref(n)))
+        return n.value
+
+    def set_params(self, p, w, b):
+        w = np.ascontiguousarray(w, dtype=np.float32)
+        b = np.ascontiguousarray(b, dtype=np.float32)
+        check(load().ce_net_set_params(self._h, p, fptr(w), fptr(b)))
+
+    def get_params(self, p, w_shape, b_shape):
+        w, b = np.empty(w_shape, np.float32), np.empty(b_shape, np.float32)
+        vw, vb = np.empty(w_shape, np.float32), np.empty(b_shape, np.float32)
+        check(load().ce_net_get_params(self._h, p, fptr(w), fptr(b), fptr(vw), fptr(vb)))
+        return w, b, vw, vb
+
+    def get_grads(self, p, w_shape, b_shape):
+        gw, gb = np.empty(w_shape, np.float32), np.empty(b_shape, np.float32)
+        check(load().ce_net_get_grads(self._h, p, fptr(gw), fptr(gb)))
+        return gw, gb
+
+    def forward(self, x, classes=2):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.empty((len(x), classes), np.float32)
+        check(load().ce_net_forward_host(self._h, fptr(x), len(x), fptr(out)))
+        return out
+
+    def activation(self, layer, n, shape):
+        out = np.empty((n, *shape), np.float32)
+        check(load().ce_net_get_activation(self._h, layer, n, fptr(out)))
+        return out
+
+    def train_batch(self, x, labels, lr, momentum):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        y = np.ascontiguousarray(labels, dtype=np.int64)
+        loss = np.zeros(1, np.float32)
+        check(load().ce_net_train_batch_host(self._h, fptr(x), y.ctypes.data_as(_I64), len(x),
+                                             float(lr), float(momentum), fptr(loss)))
+        return float(loss[0])
+
+    def train(self, dataset, perms, steps_per_epoch, batch, lr, momentum):
+        perms = np.ascontiguousarray(perms, dtype=np.int32)
+        epochs, n_perm = perms.shape
+        losses = np.zeros(epochs * steps_per_epoch, np.float32)
+        ms = C.c_double(0.0)
+        check(load().ce_train(self._h, dataset.handle, perms.ctypes.data_as(_I32), n_perm, epochs,
+                              steps_per_epoch, batch, float(lr), float(momentum), fptr(losses), C.byref(ms)))
+        return losses, ms.value
+
+    def predict(self, dataset, batch=128):
+        scores = np.empty(dataset.n, np.float64)
+        preds = np.empty(dataset.n, np.int64)
+        check(load().ce_predict(self._h, dataset.handle, batch, scores.ctypes.data_as(_D),
+                                preds.ctypes.data_as(_I64)))
+        return scores, preds
+
+    def latency(self, x, warmup, reps):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        secs = np.zeros(reps, np.float64)
+        check(load().ce_latency(self._h, fptr(x), len(x), warmup, reps, secs.ctypes.data_as(_D)))
+        return secs

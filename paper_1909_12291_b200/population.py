@@ -1,0 +1,90 @@
+"""evaluate(population): shard a population of genomes over GPUs x slots.
+
+This is the north star's "evaluate(population) returning fitness tuples":
+the GA host (ga.Master) or a fixed genome list feeds a GpuPool; each record
+comes back to the host, nothing else does (no collective).
+"""
+
+import numpy as np
+
+from .candidate import TrainBudget, evaluate
+from .genes import validate_shapes
+from .scheduler import GpuPool
+
+# rough B200 rates for ordering only (not for reporting)
+_TC_FLOPS = 4.0e14
+_HBM_BPS = 5.0e12
+_STEP_OVERHEAD_S = 2.0e-5
+
+
+def estimate_cost(genome, n_train=4000, budget=None, input_shape=(3, 100, 100)):
+    """Estimated device seconds to evaluate `genome` (LPT ordering key)."""
+    budget = budget or TrainBudget()
+    try:
+        trace = validate_shapes(genome, input_shape)
+    except Exception:
+        return 0.0
+    bs = min(genome.learn.batch_size, n_train)
+    steps = n_train // bs
+    if budget.max_batches_per_epoch is not None:
+        steps = min(steps, budget.max_batches_per_epoch)
+    steps *= budget.epochs
+    c = input_shape[0]
+    conv_flops = 0
+    for gene, (co, oh, ow) in zip(genome.feature_layers, trace.feature_shapes):
+        if hasattr(gene, "out_channels"):
+            conv_flops += 2 * gene.kernel ** 2 * c * co * oh * ow
+            c = co
+    dense = 0
+    units = trace.flat_units
+    for u in trace.head_units + (2,):
+        dense += units * u
+        units = u
+    t_step = 3 * bs * conv_flops / _TC_FLOPS + 24.0 * dense / _HBM_BPS + _STEP_OVERHEAD_S
+    return steps * t_step
+
+
+class ListMaster:
+    """Hands out a fixed genome list and keeps records (bench / scheduler tests)."""
+
+    def __init__(self, genomes):
+        self.genomes = list(genomes)
+        self._next = 0
+        self.records = {}
+
+    def issue(self, worker_id):
+        if self._next >= len(self.genomes):
+            return None
+        g = self.genomes[self._next]
+        self._next += 1
+        return g
+
+    def collect(self, record):
+        self.records[record.genome_id] = record
+
+
+def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), slots_per_gpu=2,
+                        order="lpt", precision="bf16", **evaluate_kwargs):
+    """Evaluate every genome; returns (records in input order, PoolReport)."""
+    master = ListMaster(genomes)
+    n_train = len(splits.train)
+
+    def run_one(genome, worker_id, device):
+        return evaluate(genome, splits, budget, objective, seed, worker_id=worker_id,
+                        precision=precision, device=device, **evaluate_kwargs)
+
+    pool = GpuPool(run_one, master, devices=devices, slots_per_gpu=slots_per_gpu, order=order,
+                   cost_fn=lambda g: estimate_cost(g, n_train, budget))
+    report = pool.run()
+    return [master.records.get(g.id) for g in master.genomes], report
+
+
+def shard_lpt(genomes, n_shards, cost_fn):
+    """Static longest-processing-time partition of a genome list (multi-rank bench)."""
+    loads = np.zeros(n_shards)
+    shards = [[] for _ in range(n_shards)]
+    for g in sorted(genomes, key=lambda g: -cost_fn(g)):
+        k = int(np.argmin(loads))
+        shards[k].append(g)
+        loads[k] += cost_fn(g)
+    return shards

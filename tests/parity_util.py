@@ -1,0 +1,53 @@
+"""Shared helpers for parity tests: norm-wise relative error and the genome
+cases exercised against the oracle."""
+
+import numpy as np
+
+from paper_1909_12291_b200.genes import FIXED, parse_genome
+
+
+def rel(a, b):
+    """Per-tensor ||a - b||_2 / ||b||_2 (elementwise is invalid)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    den = np.linalg.norm(b.ravel())
+    num = np.linalg.norm((a - b).ravel())
+    if den == 0.0:
+        return num
+    return num / den
+
+
+# tolerance per precision for single-kernel tensors (T1) and one step (T2)
+TOL = {"fp32": 1e-5, "bf16": 1e-2}
+
+_BASE = "parents= lr=0.001 momentum=0.9 batch_size=8 "
+
+# (name, genome text, input shape) — small inputs keep the CPU oracle fast
+CASES = [
+    ("fixed", FIXED, (3, 100, 100)),
+    ("conv_relu_pool_dense", "id=case0000000001 " + _BASE +
+     "f0=conv:oc=16,k=3,s=1,relu=1 f1=pool:size=2,s=2 f2=conv:oc=32,k=3,s=2,relu=1 h0=dense:units=24",
+     (3, 32, 32)),
+    ("pool_first_norelu", "id=case0000000002 " + _BASE +
+     "f0=pool:size=3,s=2 f1=conv:oc=8,k=5,s=1,relu=0 f2=conv:oc=64,k=2,s=3,relu=1",
+     (3, 40, 40)),
+    ("overlap_pools", "id=case0000000003 " + _BASE +
+     "f0=conv:oc=32,k=4,s=2,relu=1 f1=pool:size=3,s=1 f2=pool:size=2,s=1 f3=conv:oc=16,k=1,s=1,relu=1",
+     (3, 36, 36)),
+    ("pool_only", "id=case0000000004 " + _BASE + "f0=pool:size=2,s=2 h0=dense:units=16", (3, 20, 20)),
+    ("stride3_k7", "id=case0000000005 " + _BASE +
+     "f0=conv:oc=24,k=7,s=3,relu=1 f1=conv:oc=128,k=3,s=2,relu=1 f2=conv:oc=256,k=2,s=1,relu=0 "
+     "h0=dense:units=40", (3, 48, 48)),
+]
+
+
+def case_genome(text):
+    return parse_genome(text)
+
+
+def make_batch(n, shape, seed=0):
+    rng = np.random.default_rng(seed)
+    x = (rng.integers(0, 256, size=(n, *shape)).astype(np.float32) / np.float32(255.0))
+    y = rng.integers(0, 2, size=n).astype(np.int64)
+    y[0], y[1] = 0, 1
+    return x, y
