@@ -119,6 +119,41 @@ int ce_predict(ce_net* net, const ce_dataset* set, int batch, double* scores, in
 /* measure_latency: warmup + reps device-timed forwards of a host batch (float32 NCHW) */
 int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double* seconds);
 
+/* ---- kernel level: single passes on caller-owned device tensors (NHWC) ------
+ * Replaces Conv2d.forward / Conv2d.backward / MaxPool.forward / MaxPool.backward
+ * (nn.py:82-116, 140-167) for one layer. bf16: x/y/dy/dx/w are bf16, conv
+ * weights [c_out][kh][kw][c] (tensor-core path); fp32: all float32 (FFMA path).
+ * Gradients dw/db are always float32. `stream` is a cudaStream_t (may be 0).  */
+typedef struct ce_conv_desc {
+  int n, c, h, w;   /* input batch and NHWC geometry (c = stored channels)    */
+  int c_out;        /* conv output channels (ignored by pool)                 */
+  int kernel;       /* conv kernel / pool window                              */
+  int stride;
+  int precision;    /* CE_PREC_*                                              */
+} ce_conv_desc;
+
+size_t ce_conv_workspace_bytes(const ce_conv_desc* d);
+int ce_conv_fwd(const ce_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
+                void* stream);
+/* dx = conv^T(dy, w), optionally gated by (mask > 0) -- the ReLU backward of the
+ * layer that produced the conv input (nn.py:182-183)                          */
+int ce_conv_dgrad(const ce_conv_desc* d, const void* dy, const void* w, const void* mask, void* dx, void* workspace,
+                  size_t ws_bytes, void* stream);
+int ce_conv_wgrad(const ce_conv_desc* d, const void* x, const void* dy, float* dw, float* db, void* workspace,
+                  size_t ws_bytes, void* stream);
+int ce_maxpool_fwd(const ce_conv_desc* d, const void* x, void* y, uint8_t* arg, void* stream);
+int ce_maxpool_bwd(const ce_conv_desc* d, const void* dy, const uint8_t* arg, const void* mask, void* dx,
+                   void* stream);
+
+/* ---- instrumentation (bench.py) ------------------------------------------- */
+/* kernels this process has launched through the library (graph replays count every node) */
+long long ce_launch_count(void);
+/* per-kernel-class CUDA-event timing of ce_train (steps run un-graphed while enabled) */
+int ce_prof_num_classes(void);
+int ce_net_set_profiling(ce_net* net, int on);
+int ce_net_prof_read(ce_net* net, int cls, const char** name, long long* launches, double* ms, double* flops,
+                     double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

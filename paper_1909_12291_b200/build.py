@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libmenndl_sm100.so")
-SOURCES = ["net.cu"]
+SOURCES = ["libmenndl.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

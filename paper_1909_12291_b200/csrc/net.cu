@@ -12,6 +12,7 @@
 #include <vector>
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include "ops.cuh"
 #include "conv_tc.cuh"
 
@@ -63,8 +64,30 @@ struct ce_dataset {
   int n = 0, c = 0, h = 0, w = 0;
 };
 
+// Per-kernel-class profiling (bench.py roofline): when enabled, ce_train runs
+// its steps eagerly and brackets every launch of a class with CUDA events on
+// the launching stream; durations, algorithmic FLOPs and bytes accumulate.
+enum ProfClass { P_CONV_FWD = 0, P_CONV_DGRAD, P_CONV_WGRAD, P_CONV_SGD, P_DENSE_FWD, P_DENSE_BWD, P_POOL,
+                 P_LOSS, P_GATHER, P_NCLASS };
+static const char* kProfNames[P_NCLASS] = {"conv_fwd", "conv_dgrad", "conv_wgrad", "conv_sgd", "dense_fwd",
+                                           "dense_bwd", "pool", "loss", "gather"};
+struct ProfEvent {
+  int cls;
+  double flops, bytes;
+  cudaEvent_t a, b;
+};
+struct ProfTotals {
+  long long launches = 0;
+  double ms = 0, flops = 0, bytes = 0;
+};
+static std::atomic<long long> g_launches{0};
+
 struct ce_net {
   int device = 0, prec = CE_PREC_BF16, num_sms = 148;
+  bool prof_on = false;
+  std::vector<ProfEvent> prof_pending;
+  ProfTotals prof[P_NCLASS];
+  long long acc = 0;  // kernels enqueued since the last reset
   cudaStream_t st = nullptr;
   int in_c = 3, in_cp = 8, in_h = 100, in_w = 100, max_batch = 0, classes = 2;
   std::vector<Layer> L;
@@ -126,6 +149,45 @@ struct DevGuard {
 
 inline size_t act_bytes(const ce_net* net) { return net->prec == CE_PREC_FP32 ? 4 : 2; }
 
+struct Prof {
+  ce_net* net;
+  int cls;
+  double flops, bytes;
+  int kernels;
+  cudaEvent_t a = nullptr;
+  Prof(ce_net* n, int c, double f, double b, int k = 1) : net(n), cls(c), flops(f), bytes(b), kernels(k) {
+    net->acc += k;
+    if (net->prof_on) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, net->st);
+    }
+  }
+  ~Prof() {
+    if (net->prof_on) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecord(b, net->st);
+      net->prof_pending.push_back(ProfEvent{cls, flops, bytes, a, b});
+    }
+  }
+};
+
+void prof_collect(ce_net* net) {
+  for (auto& e : net->prof_pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(e.b);
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    ProfTotals& t = net->prof[e.cls];
+    t.launches += 1;
+    t.ms += ms;
+    t.flops += e.flops;
+    t.bytes += e.bytes;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  net->prof_pending.clear();
+}
+
 int pick_splits(long long blocks_per_split, long long K, long long min_chunk, int num_sms) {
   long long want = (2LL * num_sms + blocks_per_split - 1) / blocks_per_split;
   long long cap = K / min_chunk;
@@ -147,6 +209,9 @@ int enqueue_forward(ce_net* net, int n) {
       ConvGeom g = l.g;
       g.n = n;
       const int M = n * g.oh * g.ow, K = g.k * g.k * g.c;
+      const double ab = (double)act_bytes(net);
+      Prof pf(net, P_CONV_FWD, 2.0 * M * g.co * g.k * g.k * l.c_real,
+              ab * ((double)n * g.h * g.w * g.c + (double)M * g.co + (double)g.co * K) + 4.0 * g.co);
       if (net->use_tc) {
         int s = conv_fwd_tc(g, (const bf16*)in, l.Wbf, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
         if (s != CE_OK) return s;
@@ -158,11 +223,13 @@ int enqueue_forward(ce_net* net, int n) {
       ConvGeom g = l.g;
       g.n = n;
       size_t total = (size_t)n * g.oh * g.ow * g.c;
+      Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)n * g.h * g.w * g.c + total) + total);
       maxpool_fwd_kernel<T><<<grid_for(total), 256, 0, st>>>((const T*)in, g, (T*)l.out, l.arg);
     } else {
       const int B = n, K = l.in_units, O = l.out_units;
       long long bps = (long long)cdiv(B, SG_BM) * cdiv(O, SG_BN);
       int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms));
+      Prof pf(net, P_DENSE_FWD, 2.0 * B * K * O, 4.0 * K * O + (in_act ? act_bytes(net) : 4.0) * B * K, 2);
       PartialEpi pe{net->ws, B, O};
       if (in_act)
         simt_gemm(DenseXA<T>{(const T*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
@@ -204,6 +271,9 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
     if (l.kind == CE_LAYER_DENSE) {
       const int B = n, K = l.in_units, O = l.out_units;
       const float* g = (const float*)gin;
+      Prof pf(net, P_DENSE_BWD, (l.need_dx ? 4.0 : 2.0) * B * K * O,
+              (l.need_dx ? 24.0 : 20.0) * K * O + 2.0 * (l.in_is_act ? act_bytes(net) : 4.0) * B * K,
+              l.need_dx ? 4 : 3);
       if (l.need_dx) {
         if (l.in_is_act)
           simt_gemm(DenseGA{g, O}, DenseWN{l.W, K}, DenseDxEpi<T, T>{(T*)gout, mask, K}, B, K, O, 1, st);
@@ -227,7 +297,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       g.n = n;
       const T* dy = (const T*)gin;
       const int Mo = n * g.oh * g.ow, K = g.k * g.k * g.c;
+      const double ab = (double)act_bytes(net);
+      const double useful = 2.0 * Mo * g.co * g.k * g.k * l.c_real;
       if (l.need_dx) {
+        Prof pf(net, P_CONV_DGRAD, useful,
+                ab * ((double)Mo * g.co + (double)g.co * K + 2.0 * n * g.h * g.w * g.c));
         if (net->use_tc) {
           int s = conv_dgrad_tc(g, (const bf16*)dy, l.Wtbf, (const bf16*)mask, (bf16*)gout, net->num_sms, st);
           if (s != CE_OK) return s;
@@ -238,9 +312,12 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         CE_CHECK_LAUNCH();
       }
       int splits;
+      {
+      Prof pf(net, P_CONV_WGRAD, useful, ab * ((double)Mo * g.co + (double)n * g.h * g.w * g.c));
       if (net->use_tc) {
         int s = conv_wgrad_tc(g, (const bf16*)x, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
+        pf.bytes += 4.0 * splits * g.co * K;
       } else {
         long long bps = (long long)cdiv(g.co, SG_BM) * cdiv(K, SG_BN);
         splits = simt_splits(Mo, pick_splits(bps, Mo, 512, net->num_sms));
@@ -248,9 +325,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
                   splits, st);
       }
       CE_CHECK_LAUNCH();
+      }
       float* bpart = net->ws + (size_t)splits * g.co * K;
       int bsplits = std::min(64, std::max(1, Mo / 2048));
       int mchunk = cdiv(Mo, bsplits);
+      Prof pf(net, P_CONV_SGD, 0.0, ab * Mo * g.co + 4.0 * splits * g.co * K + 20.0 * g.co * K, 3);
       colsum_partial_kernel<T><<<dim3(cdiv(g.co, 128), bsplits), 128, 0, st>>>(dy, Mo, g.co, mchunk, bpart);
       conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(net->ws, splits, g.co, K, g.c, g.k * g.k, l.W, l.VW,
                                                                    keep ? l.GW : nullptr, l.Wbf, l.Wtbf, lr, mu);
@@ -261,6 +340,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         ConvGeom g = l.g;
         g.n = n;
         size_t total = (size_t)n * g.h * g.w * g.c;
+        Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)n * g.oh * g.ow * g.c * 2 + total));
         maxpool_bwd_kernel<T, T><<<grid_for(total), 256, 0, st>>>((const T*)gin, l.arg, g, mask, (T*)gout);
         CE_CHECK_LAUNCH();
       }
@@ -276,6 +356,7 @@ int enqueue_step(ce_net* net, int n, float lr, float mu) {
   int s = enqueue_forward<T>(net, n);
   if (s != CE_OK) return s;
   const Layer& last = net->L.back();
+  Prof pf(net, P_LOSS, 0.0, 16.0 * n * net->classes);
   xent_kernel<<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes, (float*)net->gbuf[0],
                                         net->d_losses, net->d_step);
   CE_CHECK_LAUNCH();
@@ -293,6 +374,7 @@ int gather_any(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_per
                bool labels) {
   dim3 grid(cdiv(ds->h * ds->w, 256), B);
   int HW = ds->h * ds->w;
+  Prof pf(net, P_GATHER, 0.0, (double)B * HW * (ds->c + net->in_cp * act_bytes(net)));
   if (net->prec == CE_PREC_FP32)
     gather_u8_kernel<float><<<grid, 256, 0, net->st>>>(ds->pix, ds->lab, perm, net->d_step, n_perm, spe, base, B,
                                                        ds->c, net->in_cp, HW, (float*)net->x0,
@@ -318,6 +400,7 @@ int upload_host_batch(ce_net* net, const float* x, int n) {
   CE_CUDA(cudaMemcpyAsync(net->d_xhost, x, elems * 4, cudaMemcpyHostToDevice, net->st));
   int HW = net->in_h * net->in_w;
   size_t total = (size_t)n * HW;
+  net->acc += 1;
   if (net->prec == CE_PREC_FP32)
     nchw_to_nhwc_kernel<float><<<grid_for(total), 256, 0, net->st>>>(net->d_xhost, n, net->in_c, net->in_cp, HW,
                                                                       (float*)net->x0);
@@ -339,6 +422,28 @@ int check_net(const ce_net* net) {
 extern "C" {
 
 int ce_version(void) { return 1; }
+long long ce_launch_count(void) { return g_launches.load(); }
+int ce_prof_num_classes(void) { return P_NCLASS; }
+
+int ce_net_set_profiling(ce_net* net, int on) {
+  if (!net) return fail(CE_EINVAL, "null net");
+  net->prof_on = on != 0;
+  if (on)
+    for (auto& t : net->prof) t = ProfTotals();
+  return CE_OK;
+}
+
+int ce_net_prof_read(ce_net* net, int cls, const char** name, long long* launches, double* ms, double* flops,
+                     double* bytes) {
+  if (!net || cls < 0 || cls >= P_NCLASS) return fail(CE_EINVAL, "bad profile class %d", cls);
+  const ProfTotals& t = net->prof[cls];
+  if (name) *name = kProfNames[cls];
+  if (launches) *launches = t.launches;
+  if (ms) *ms = t.ms;
+  if (flops) *flops = t.flops;
+  if (bytes) *bytes = t.bytes;
+  return CE_OK;
+}
 const char* ce_last_error(void) { return g_err; }
 
 int ce_device_count(int* count) {
@@ -747,11 +852,13 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   }
   CE_CUDA(cudaMemcpyAsync(net->d_perm, perm, pn * 4, cudaMemcpyHostToDevice, st));
   CE_CUDA(cudaMemsetAsync(net->d_step, 0, 4, st));
-  // capture one step
+  // capture one step (profiling runs eagerly so each launch can be bracketed)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   bool graphed = false;
-  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+  net->acc = 0;
+  long long per_step = 0;
+  if (!net->prof_on && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
     int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true);
     if (s == CE_OK) s = step_any(net, batch, lr, momentum);
     cudaError_t ce = cudaStreamEndCapture(st, &graph);
@@ -761,8 +868,10 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
     }
     if (ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) graphed = true;
     if (graph) cudaGraphDestroy(graph);
+    per_step = net->acc;
   }
   cudaGetLastError();
+  net->acc = 0;
   cudaEvent_t e0, e1;
   CE_CUDA(cudaEventCreate(&e0));
   CE_CUDA(cudaEventCreate(&e1));
@@ -775,10 +884,12 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
       if (int s = step_any(net, batch, lr, momentum)) return s;
     }
   }
+  g_launches += graphed ? per_step * steps : net->acc;
   CE_CUDA(cudaEventRecord(e1, st));
   CE_CUDA(cudaMemcpyAsync(losses, net->d_losses, (size_t)steps * 4, cudaMemcpyDeviceToHost, st));
   cudaError_t se = cudaStreamSynchronize(st);
   if (exec) cudaGraphExecDestroy(exec);
+  if (net->prof_on) prof_collect(net);
   if (se != cudaSuccess) return fail(CE_ECUDA, "train loop: %s", cudaGetErrorString(se));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -798,14 +909,17 @@ int ce_predict(ce_net* net, const ce_dataset* ds, int batch, double* scores, int
     ALLOC(net->d_preds, (size_t)ds->n * 8);
     net->pred_cap = ds->n;
   }
+  net->acc = 0;
   for (int start = 0; start < ds->n; start += batch) {
     int nb = std::min(batch, ds->n - start);
     if (int s = gather_any(net, ds, nullptr, 0, 1, start, nb, false)) return s;
     if (int s = forward_any(net, nb)) return s;
+    net->acc += 1;
     predict_head_kernel<<<cdiv(nb, 128), 128, 0, st>>>((const float*)net->L.back().out, nb, net->classes, start,
                                                         net->d_scores, net->d_preds);
     CE_CHECK_LAUNCH();
   }
+  g_launches += net->acc;
   CE_CUDA(cudaMemcpyAsync(scores, net->d_scores, (size_t)ds->n * 8, cudaMemcpyDeviceToHost, st));
   CE_CUDA(cudaMemcpyAsync(preds, net->d_preds, (size_t)ds->n * 8, cudaMemcpyDeviceToHost, st));
   CE_CUDA(cudaStreamSynchronize(st));
@@ -817,6 +931,7 @@ int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double*
   if (n < 1 || n > net->max_batch || warmup < 0 || reps < 1) return fail(CE_EINVAL, "ce_latency: bad arguments");
   DevGuard dg(net->device);
   cudaStream_t st = net->st;
+  net->acc = 0;
   if (int s = upload_host_batch(net, x, n)) return s;
   for (int i = 0; i < warmup; ++i)
     if (int s = forward_any(net, n)) return s;
@@ -827,6 +942,7 @@ int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double*
     if (int s = forward_any(net, n)) return s;
     CE_CUDA(cudaEventRecord(ev[2 * r + 1], st));
   }
+  g_launches += net->acc;
   CE_CUDA(cudaStreamSynchronize(st));
   for (int r = 0; r < reps; ++r) {
     float ms = 0.f;

@@ -136,6 +136,7 @@ __global__ void conv_sgd_kernel(const float* __restrict__ part, int splits, int 
     float g = 0.f;
     for (int s = 0; s < splits; ++s) g += part[(size_t)s * total + e];
     if (gw) gw[e] = g;
+    if (!w) continue;  // reduction only (kernel-level wgrad)
     float wv = w[e], vv = vel[e];
     sgd_update(wv, vv, g, lr, mu);
     w[e] = wv;
@@ -157,6 +158,7 @@ __global__ void bias_sgd_kernel(const float* __restrict__ part, int splits, int 
   float g = 0.f;
   for (int s = 0; s < splits; ++s) g += part[(size_t)s * n + o];
   if (gb) gb[o] = g;
+  if (!b) return;
   float bv = b[o], vv = vel[o];
   sgd_update(bv, vv, g, lr, mu);
   b[o] = bv;
@@ -294,6 +296,18 @@ __global__ void conv_wt_kernel(const float* __restrict__ w, int co, int taps, in
     int tap = t % taps;
     int o = t / taps;
     wt[((size_t)c * taps + tap) * co + o] = __float2bfloat16_rn(w[e]);
+  }
+}
+
+// bf16 [o][tap][c] -> [c][tap][o] (dgrad B operand)
+__global__ void transpose_w_bf16_kernel(const bf16* __restrict__ w, int co, int taps, int cp, bf16* __restrict__ wt) {
+  size_t total = (size_t)co * taps * cp;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int c = e % cp;
+    size_t t = e / cp;
+    int tap = t % taps;
+    int o = t / taps;
+    wt[((size_t)c * taps + tap) * co + o] = w[e];
   }
 }
 

@@ -30,6 +30,11 @@ class NetDesc(C.Structure):
                 ("layers", C.POINTER(LayerDesc)), ("max_batch", C.c_int)]
 
 
+class ConvDesc(C.Structure):
+    _fields_ = [("n", C.c_int), ("c", C.c_int), ("h", C.c_int), ("w", C.c_int), ("c_out", C.c_int),
+                ("kernel", C.c_int), ("stride", C.c_int), ("precision", C.c_int)]
+
+
 _P = C.c_void_p
 _F = C.POINTER(C.c_float)
 _D = C.POINTER(C.c_double)
@@ -56,6 +61,16 @@ _SIGNATURES = {
     "ce_train": ([_P, _P, _I32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float, _F, _D], C.c_int),
     "ce_predict": ([_P, _P, C.c_int, _D, _I64], C.c_int),
     "ce_latency": ([_P, _F, C.c_int, C.c_int, C.c_int, _D], C.c_int),
+    "ce_conv_workspace_bytes": ([C.POINTER(ConvDesc)], C.c_size_t),
+    "ce_conv_fwd": ([C.POINTER(ConvDesc), _P, _P, _P, C.c_int, _P, _P], C.c_int),
+    "ce_conv_dgrad": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "ce_conv_wgrad": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "ce_maxpool_fwd": ([C.POINTER(ConvDesc), _P, _P, _P, _P], C.c_int),
+    "ce_maxpool_bwd": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P], C.c_int),
+    "ce_launch_count": ([], C.c_longlong),
+    "ce_prof_num_classes": ([], C.c_int),
+    "ce_net_set_profiling": ([_P, C.c_int], C.c_int),
+    "ce_net_prof_read": ([_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_longlong), _D, _D, _D], C.c_int),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -94,6 +109,39 @@ def check(status):
 
 def fptr(a):
     return a.ctypes.data_as(_F) if a is not None else None
+
+
+def conv_desc(n, c, h, w, c_out, kernel, stride, precision):
+    return ConvDesc(n, c, h, w, c_out, kernel, stride, PRECISIONS[precision])
+
+
+def conv_workspace_bytes(desc):
+    return int(load().ce_conv_workspace_bytes(C.byref(desc)))
+
+
+def conv_fwd(desc, x, w, bias, relu, y, stream=0):
+    """Kernel-level conv forward on device pointers (ints) of NHWC tensors."""
+    check(load().ce_conv_fwd(C.byref(desc), x, w, bias, int(relu), y, stream))
+
+
+def conv_dgrad(desc, dy, w, mask, dx, ws, ws_bytes, stream=0):
+    check(load().ce_conv_dgrad(C.byref(desc), dy, w, mask, dx, ws, ws_bytes, stream))
+
+
+def conv_wgrad(desc, x, dy, dw, db, ws, ws_bytes, stream=0):
+    check(load().ce_conv_wgrad(C.byref(desc), x, dy, dw, db, ws, ws_bytes, stream))
+
+
+def maxpool_fwd(desc, x, y, arg, stream=0):
+    check(load().ce_maxpool_fwd(C.byref(desc), x, y, arg, stream))
+
+
+def maxpool_bwd(desc, dy, arg, mask, dx, stream=0):
+    check(load().ce_maxpool_bwd(C.byref(desc), dy, arg, mask, dx, stream))
+
+
+def launch_count():
+    return int(load().ce_launch_count())
 
 
 def device_count():
@@ -214,6 +262,20 @@ class Net:
         check(load().ce_predict(self._h, dataset.handle, batch, scores.ctypes.data_as(_D),
                                 preds.ctypes.data_as(_I64)))
         return scores, preds
+
+    def set_profiling(self, on):
+        check(load().ce_net_set_profiling(self._h, int(bool(on))))
+
+    def profile(self):
+        """Per kernel class: {name: (launches, ms, flops, bytes)} accumulated by ce_train."""
+        lib, out = load(), {}
+        for cls in range(lib.ce_prof_num_classes()):
+            name, n = C.c_char_p(), C.c_longlong()
+            ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+            check(lib.ce_net_prof_read(self._h, cls, C.byref(name), C.byref(n), C.byref(ms), C.byref(fl),
+                                       C.byref(by)))
+            out[name.value.decode()] = (n.value, ms.value, fl.value, by.value)
+        return out
 
     def latency(self, x, warmup, reps):
         x = np.ascontiguousarray(x, dtype=np.float32)

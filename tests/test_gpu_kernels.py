@@ -1,0 +1,111 @@
+"""T1 kernel parity through the kernel-level C ABI on bf16-exact inputs.
+
+Inputs and weights are rounded to bf16 first, so the oracle (float64 on the
+same values) and the tcgen05 kernels see identical operands; the remaining
+error is fp32 accumulation + the bf16 rounding of stored outputs. This is the
+per-kernel bar of north_star (rel <= 1e-2 bf16, <= 1e-5 fp32 check mode);
+pooling is exact.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import cnn_ref as O
+from paper_1909_12291_b200 import native
+
+from parity_util import rel
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+# (n, c, h, c_out, k, s): FIXED layers (c padded 3->8), SWEET-like, random-genome-like
+SHAPES = [(4, 8, 100, 32, 4, 2), (4, 32, 49, 64, 4, 1), (4, 64, 23, 128, 4, 1), (2, 256, 19, 256, 4, 1),
+          (3, 16, 33, 8, 1, 2), (2, 8, 40, 24, 7, 3), (2, 128, 16, 256, 2, 3), (5, 64, 17, 16, 5, 2),
+          (2, 32, 12, 64, 3, 3), (1, 16, 9, 128, 6, 1), (2, 24, 11, 40, 3, 2)]
+
+
+def _round(a, precision):
+    if precision == "fp32":
+        return a.astype(np.float32)
+    return torch.from_numpy(a.astype(np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def _dev(a_nhwc, precision):
+    t = torch.from_numpy(np.ascontiguousarray(a_nhwc, dtype=np.float32)).cuda()
+    return t.to(torch.bfloat16).contiguous() if precision == "bf16" else t.contiguous()
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("shape", SHAPES, ids=[str(s) for s in SHAPES])
+def test_conv_passes(shape, precision):
+    n, c, h, co, k, s = shape
+    rng = np.random.default_rng(sum(shape))
+    x = _round(rng.standard_normal((n, c, h, h)), precision)
+    w = _round(rng.uniform(-0.2, 0.2, (co, c, k, k)), precision)
+    b = rng.uniform(-0.1, 0.1, co).astype(np.float32)
+    oh = (h - k) // s + 1
+    dy = _round(rng.standard_normal((n, co, oh, oh)), precision)
+    mask_src = rng.standard_normal((n, c, h, h)).astype(np.float32)
+    # oracle in float64 on the same (rounded) values
+    y_ref = O.conv_forward(x.astype(np.float64), w.astype(np.float64), b.astype(np.float64), s)
+    y_ref = np.maximum(y_ref, 0)
+    dx_ref, dw_ref, db_ref = O.conv_backward(x.astype(np.float64), w.astype(np.float64), s, dy.astype(np.float64))
+    dx_ref = dx_ref * (mask_src > 0)
+
+    desc = native.conv_desc(n, c, h, h, co, k, s, precision)
+    xd = _dev(x.transpose(0, 2, 3, 1), precision)
+    wd = _dev(w.transpose(0, 2, 3, 1), precision)           # [o][kh][kw][c]
+    bd = torch.from_numpy(b).cuda()
+    yd = torch.empty((n, oh, oh, co), dtype=xd.dtype, device="cuda")
+    dyd = _dev(dy.transpose(0, 2, 3, 1), precision)
+    maskd = _dev(mask_src.transpose(0, 2, 3, 1), precision)
+    dxd = torch.empty_like(xd)
+    dwd = torch.empty((co, k, k, c), dtype=torch.float32, device="cuda")
+    dbd = torch.empty(co, dtype=torch.float32, device="cuda")
+    wsb = native.conv_workspace_bytes(desc)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    native.conv_fwd(desc, xd.data_ptr(), wd.data_ptr(), bd.data_ptr(), 1, yd.data_ptr(), st)
+    native.conv_dgrad(desc, dyd.data_ptr(), wd.data_ptr(), maskd.data_ptr(), dxd.data_ptr(), ws.data_ptr(), wsb, st)
+    native.conv_wgrad(desc, xd.data_ptr(), dyd.data_ptr(), dwd.data_ptr(), dbd.data_ptr(), ws.data_ptr(), wsb, st)
+    torch.cuda.synchronize()
+    tol = 1e-2 if precision == "bf16" else 1e-5
+    y = yd.float().cpu().numpy().transpose(0, 3, 1, 2)
+    dx = dxd.float().cpu().numpy().transpose(0, 3, 1, 2)
+    dw = dwd.cpu().numpy().transpose(0, 3, 1, 2)
+    assert rel(y, y_ref) <= tol, f"fwd rel err {rel(y, y_ref):.3e}"
+    assert rel(dx, dx_ref) <= tol, f"dgrad rel err {rel(dx, dx_ref):.3e}"
+    assert rel(dw, dw_ref) <= tol, f"wgrad rel err {rel(dw, dw_ref):.3e}"
+    assert rel(dbd.cpu().numpy(), db_ref) <= tol
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("size,stride", [(2, 1), (2, 2), (2, 3), (3, 1), (3, 2), (3, 3)])
+@pytest.mark.parametrize("variant", ["rand", "ties"])
+def test_pool_exact(size, stride, variant, precision):
+    rng = np.random.default_rng(size * 7 + stride)
+    n, c, h = 3, 16, 13
+    if variant == "rand":
+        x = _round(rng.standard_normal((n, c, h, h)), precision)
+    else:
+        x = rng.integers(0, 3, size=(n, c, h, h)).astype(np.float32)
+    oh = (h - size) // stride + 1
+    dy = _round(rng.standard_normal((n, c, oh, oh)), precision)
+    y_ref, arg_ref = O.pool_forward(x, size, stride)
+    dx_ref = O.pool_backward(dy.astype(np.float64), arg_ref, x.shape, size, stride)
+    desc = native.conv_desc(n, c, h, h, 0, size, stride, precision)
+    xd = _dev(x.transpose(0, 2, 3, 1), precision)
+    yd = torch.empty((n, oh, oh, c), dtype=xd.dtype, device="cuda")
+    argd = torch.empty((n, oh, oh, c), dtype=torch.uint8, device="cuda")
+    dyd = _dev(dy.transpose(0, 2, 3, 1), precision)
+    dxd = torch.empty_like(xd)
+    native.maxpool_fwd(desc, xd.data_ptr(), yd.data_ptr(), argd.data_ptr())
+    native.maxpool_bwd(desc, dyd.data_ptr(), argd.data_ptr(), None, dxd.data_ptr())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(yd.float().cpu().numpy().transpose(0, 3, 1, 2), y_ref)
+    np.testing.assert_array_equal(argd.cpu().numpy().transpose(0, 3, 1, 2), arg_ref)
+    dx = dxd.float().cpu().numpy().transpose(0, 3, 1, 2)
+    if precision == "fp32" or size <= stride:  # no overlap: a single term per input, exact
+        assert rel(dx, dx_ref) <= 1e-6
+    else:  # overlapping windows accumulate in fp32 then round to bf16
+        assert rel(dx, dx_ref) <= 1e-2
