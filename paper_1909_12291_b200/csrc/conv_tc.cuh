@@ -6,7 +6,8 @@
 //   fwd  : D[(n,p,q)][o]  = sum_{(i,j,c)} x[n, sp+i, sq+j, c] * W[o][i][j][c]      A,B K-major
 //          epilogue: + bias, ReLU, bf16 NHWC store                 (nn.py:82-94, 178-180)
 //   dgrad: D[(n,h,w)][c]  = sum_{(i,j,o)} dy[n, (h-i)/s, (w-j)/s, o] * Wt[c][i][j][o]   A,B K-major
-//          invalid taps (not on the stride lattice / out of range) are zero-filled;
+//          one stride-1 GEMM per residue class (h mod s, w mod s) over that class's
+//          taps only (sub-pixel decomposition); out-of-range taps are zero-filled;
 //          epilogue: x ReLU mask of the input activation, bf16 store  (nn.py:112-113, 183)
 //   wgrad: D[(i,j,c)][o]  = sum_{(n,p,q)} x[n, sp+i, sq+j, c] * dy[n,p,q,o]           A,B MN-major
 //          reduction split across CTAs; epilogue writes fp32 partials part[split][o][(i,j,c)]
@@ -92,24 +93,36 @@ struct FwdTcEpi {
 };
 
 // ------------------------------------------------------------------ dgrad
+// Sub-pixel decomposition: input positions (h, w) = (rh + s*hh, rw + s*ww) of one
+// residue class (rh, rw) only receive taps i = rh + s*a, j = rw + s*b, from
+// dy[n, hh - a, ww - b]; each class is a dense stride-1 implicit GEMM with
+// K = ti*tj*C_out, so no MMA work is spent on off-lattice taps.
+struct DgradClass {
+  int rh, rw;   // residue class
+  int ti, tj;   // valid taps per axis
+  int hc, wc;   // positions of the class per axis
+};
+
 struct DgradTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
   const bf16* dy;
-  const bf16* wt;  // [c][k*k*co]
+  const bf16* wt;  // [c][k*k][co]
   ConvGeom g;
-  int K, M, BN;
+  DgradClass cl;
+  int K, M, BN;    // K = ti*tj*co, M = n*hc*wc
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid) const {
     {
       const int r = ptid;
       const int m = c.m0 + r;
       const bool row_ok = m < M;
-      int wx = 0, hy = 0, n = 0;
+      int ww = 0, hh = 0, n = 0;
       if (row_ok) {
-        wx = m % g.w;
-        int t = m / g.w;
-        hy = t % g.h;
-        n = t / g.h;
+        ww = m % cl.wc;
+        int t = m / cl.wc;
+        hh = t % cl.hc;
+        n = t / cl.hc;
       }
+      const bf16* row = dy + (((size_t)n * g.oh + hh) * g.ow + ww) * g.co;
 #pragma unroll
       for (int kc = 0; kc < 8; ++kc) {
         const int kk = kb * TC_BK + kc * 8;
@@ -117,13 +130,9 @@ struct DgradTcLoader {
         const bf16* src = dy;
         if (ok) {
           const int tap = kk / g.co, o0 = kk - tap * g.co;
-          const int i = tap / g.k, j = tap - i * g.k;
-          int hp = hy - i, wq = wx - j;
-          ok = hp >= 0 && wq >= 0 && (hp % g.s) == 0 && (wq % g.s) == 0;
-          hp /= g.s;
-          wq /= g.s;
-          ok = ok && hp < g.oh && wq < g.ow;
-          if (ok) src = dy + (((size_t)n * g.oh + hp) * g.ow + wq) * g.co + o0;
+          const int a = tap / cl.tj, b = tap - a * cl.tj;
+          ok = hh >= a && ww >= b && hh - a < g.oh && ww - b < g.ow;
+          if (ok) src = row - ((size_t)a * g.ow + b) * g.co + o0;
         }
         cp_async16(sA + kmajor_off(TC_BM, r, kc), src, ok ? 16u : 0u);
       }
@@ -132,8 +141,14 @@ struct DgradTcLoader {
       const int r = ch % BN, kc = ch / BN;
       const int cc = c.n0 + r, kk = kb * TC_BK + kc * 8;
       const bool ok = cc < g.c && kk < K;
-      cp_async16(sB + kmajor_off(BN, r, kc), ok ? (const void*)(wt + (size_t)cc * K + kk) : (const void*)wt,
-                 ok ? 16u : 0u);
+      const bf16* src = wt;
+      if (ok) {
+        const int tap = kk / g.co, o0 = kk - tap * g.co;
+        const int a = tap / cl.tj, b = tap - a * cl.tj;
+        const int i = cl.rh + g.s * a, j = cl.rw + g.s * b;
+        src = wt + ((size_t)cc * g.k * g.k + i * g.k + j) * g.co + o0;
+      }
+      cp_async16(sB + kmajor_off(BN, r, kc), src, ok ? 16u : 0u);
     }
   }
 };
@@ -141,26 +156,31 @@ struct DgradTcLoader {
 struct DgradTcEpi {
   bf16* dx;
   const bf16* mask;
-  int M, c;
+  ConvGeom g;
+  DgradClass cl;
+  int M;
   __device__ void store(const TileCoord& tc, int row, int col, const float (&v)[16]) const {
     const int m = tc.m0 + row;
     const int c0 = tc.n0 + col;
-    if (m >= M || c0 >= c) return;
-    const size_t off = (size_t)m * c + c0;
+    if (m >= M || c0 >= g.c) return;
+    const int ww = m % cl.wc;
+    const int t = m / cl.wc;
+    const int hh = t % cl.hc, n = t / cl.hc;
+    const size_t off = (((size_t)n * g.h + cl.rh + g.s * hh) * g.w + cl.rw + g.s * ww) * g.c + c0;
     __align__(16) bf16 out[16];
     __align__(16) bf16 mk[16];
     if (mask) {
       *(uint4*)&mk[0] = *(const uint4*)(mask + off);
-      if (c0 + 8 < c) *(uint4*)&mk[8] = *(const uint4*)(mask + off + 8);
+      if (c0 + 8 < g.c) *(uint4*)&mk[8] = *(const uint4*)(mask + off + 8);
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float t = v[i];
-      if (mask && !(__bfloat162float(mk[i]) > 0.f)) t = 0.f;
-      out[i] = __float2bfloat16_rn(t);
+      float t2 = v[i];
+      if (mask && !(__bfloat162float(mk[i]) > 0.f)) t2 = 0.f;
+      out[i] = __float2bfloat16_rn(t2);
     }
     *(uint4*)(dx + off) = *(const uint4*)&out[0];
-    if (c0 + 8 < c) *(uint4*)(dx + off + 8) = *(const uint4*)&out[8];
+    if (c0 + 8 < g.c) *(uint4*)(dx + off + 8) = *(const uint4*)&out[8];
   }
   __device__ void finish(int, int) const {}
 };
@@ -254,15 +274,36 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
 
 inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, const bf16* mask, bf16* dx, int num_sms,
                          cudaStream_t st) {
-  const int M = g.n * g.h * g.w, K = g.k * g.k * g.co;
-  return with_bn(g.c, [&](auto bn) {
-    constexpr int BN = decltype(bn)::value;
-    TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
-    DgradTcLoader ld{dy, wt, g, K, M, BN};
-    DgradTcEpi ep{dx, mask, M, g.c};
-    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
-    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_dgrad_tc: %s", cudaGetErrorString(e));
-  });
+  bool any_empty = false;
+  for (int rh = 0; rh < g.s && rh < g.h; ++rh)
+    for (int rw = 0; rw < g.s && rw < g.w; ++rw)
+      if (rh >= g.k || rw >= g.k) any_empty = true;
+  if (any_empty) {  // positions no tap reaches get a zero gradient (k < s)
+    cudaError_t e = cudaMemsetAsync(dx, 0, (size_t)g.n * g.h * g.w * g.c * sizeof(bf16), st);
+    if (e != cudaSuccess) return fail(CE_ECUDA, "conv_dgrad_tc memset: %s", cudaGetErrorString(e));
+  }
+  for (int rh = 0; rh < g.s && rh < g.h; ++rh)
+    for (int rw = 0; rw < g.s && rw < g.w; ++rw) {
+      DgradClass cl;
+      cl.rh = rh;
+      cl.rw = rw;
+      cl.ti = rh < g.k ? (g.k - rh + g.s - 1) / g.s : 0;
+      cl.tj = rw < g.k ? (g.k - rw + g.s - 1) / g.s : 0;
+      cl.hc = (g.h - rh + g.s - 1) / g.s;
+      cl.wc = (g.w - rw + g.s - 1) / g.s;
+      if (cl.ti == 0 || cl.tj == 0) continue;
+      const int M = g.n * cl.hc * cl.wc, K = cl.ti * cl.tj * g.co;
+      int s = with_bn(g.c, [&](auto bn) {
+        constexpr int BN = decltype(bn)::value;
+        TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
+        DgradTcLoader ld{dy, wt, g, cl, K, M, BN};
+        DgradTcEpi ep{dx, mask, g, cl, M};
+        cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+        return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_dgrad_tc: %s", cudaGetErrorString(e));
+      });
+      if (s != CE_OK) return s;
+    }
+  return CE_OK;
 }
 
 inline int conv_wgrad_splits(const ConvGeom& g, int n, int num_sms) {

@@ -14,7 +14,8 @@ int check_desc(const ce_conv_desc* d, bool conv) {
   if (d->n < 1 || d->c < 1 || d->h < 1 || d->w < 1 || d->kernel < 1 || d->stride < 1)
     return fail(CE_EINVAL, "bad conv/pool descriptor");
   if (d->h < d->kernel || d->w < d->kernel) return fail(CE_EINVAL, "window %d exceeds input %dx%d", d->kernel, d->h, d->w);
-  if (conv && (d->c % 8 || d->c_out % 8 || d->c_out < 8))
+  if (d->c % 8) return fail(CE_EINVAL, "stored channels must be a multiple of 8 (got %d)", d->c);
+  if (conv && (d->c_out % 8 || d->c_out < 8))
     return fail(CE_EINVAL, "conv channels must be multiples of 8 (got %d -> %d)", d->c, d->c_out);
   if (d->precision != CE_PREC_BF16 && d->precision != CE_PREC_FP32) return fail(CE_EINVAL, "bad precision");
   return CE_OK;
@@ -44,7 +45,7 @@ int sms() {
 size_t wgrad_ws(const ConvGeom& g, bool tc) {
   const int K = g.k * g.k * g.c, Mo = g.n * g.oh * g.ow;
   int splits = tc ? conv_wgrad_splits(g, g.n, sms()) : simt_splits(Mo, 8);
-  return (size_t)splits * g.co * K * 4 + (size_t)64 * g.co * 4 + 256;
+  return (size_t)splits * g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * g.co * 4 + 256;
 }
 
 }  // namespace
@@ -118,14 +119,7 @@ int ce_conv_wgrad(const ce_conv_desc* d, const void* x, const void* dy, float* d
   }
   CE_CHECK_LAUNCH();
   float* bpart = part + (size_t)splits * g.co * K;
-  int bsplits = Mo / 2048 < 1 ? 1 : (Mo / 2048 > 64 ? 64 : Mo / 2048);
-  int mchunk = cdiv(Mo, bsplits);
-  if (tc)
-    colsum_partial_kernel<bf16><<<dim3(cdiv(g.co, 128), bsplits), 128, 0, st>>>((const bf16*)dy, Mo, g.co, mchunk,
-                                                                                 bpart);
-  else
-    colsum_partial_kernel<float><<<dim3(cdiv(g.co, 128), bsplits), 128, 0, st>>>((const float*)dy, Mo, g.co, mchunk,
-                                                                                  bpart);
+  const int bsplits = tc ? colsum((const bf16*)dy, Mo, g.co, bpart, st) : colsum((const float*)dy, Mo, g.co, bpart, st);
   conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(part, splits, g.co, K, g.c, g.k * g.k, nullptr, nullptr,
                                                                dw, nullptr, nullptr, 0.f, 0.f);
   bias_sgd_kernel<<<cdiv(g.co, 256), 256, 0, st>>>(bpart, bsplits, g.co, nullptr, nullptr, db, 0.f, 0.f);
@@ -139,9 +133,9 @@ int ce_maxpool_fwd(const ce_conv_desc* d, const void* x, void* y, uint8_t* arg, 
   size_t total = (size_t)g.n * g.oh * g.ow * g.c;
   cudaStream_t st = (cudaStream_t)stream;
   if (d->precision == CE_PREC_BF16)
-    maxpool_fwd_kernel<bf16><<<grid_for(total), 256, 0, st>>>((const bf16*)x, g, (bf16*)y, arg);
+    maxpool_fwd_kernel<bf16><<<grid_for(total / 8), 256, 0, st>>>((const bf16*)x, g, (bf16*)y, arg);
   else
-    maxpool_fwd_kernel<float><<<grid_for(total), 256, 0, st>>>((const float*)x, g, (float*)y, arg);
+    maxpool_fwd_kernel<float><<<grid_for(total / 8), 256, 0, st>>>((const float*)x, g, (float*)y, arg);
   CE_CHECK_LAUNCH();
   return CE_OK;
 }
@@ -153,10 +147,10 @@ int ce_maxpool_bwd(const ce_conv_desc* d, const void* dy, const uint8_t* arg, co
   size_t total = (size_t)g.n * g.h * g.w * g.c;
   cudaStream_t st = (cudaStream_t)stream;
   if (d->precision == CE_PREC_BF16)
-    maxpool_bwd_kernel<bf16, bf16><<<grid_for(total), 256, 0, st>>>((const bf16*)dy, arg, g, (const bf16*)mask,
+    maxpool_bwd_kernel<bf16, bf16><<<grid_for(total / 8), 256, 0, st>>>((const bf16*)dy, arg, g, (const bf16*)mask,
                                                                      (bf16*)dx);
   else
-    maxpool_bwd_kernel<float, float><<<grid_for(total), 256, 0, st>>>((const float*)dy, arg, g, (const float*)mask,
+    maxpool_bwd_kernel<float, float><<<grid_for(total / 8), 256, 0, st>>>((const float*)dy, arg, g, (const float*)mask,
                                                                        (float*)dx);
   CE_CHECK_LAUNCH();
   return CE_OK;

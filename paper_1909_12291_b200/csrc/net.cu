@@ -149,6 +149,18 @@ struct DevGuard {
 
 inline size_t act_bytes(const ce_net* net) { return net->prec == CE_PREC_FP32 ? 4 : 2; }
 
+// The stream-ordered pool returns freed memory to the OS at every sync by
+// default; candidates come and go every few ms, so keep it cached instead.
+void keep_pool_memory(int device) {
+  static std::atomic<unsigned> done{0};
+  if (device < 0 || device >= 32 || (done.fetch_or(1u << device) & (1u << device))) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
 struct Prof {
   ce_net* net;
   int cls;
@@ -224,7 +236,7 @@ int enqueue_forward(ce_net* net, int n) {
       g.n = n;
       size_t total = (size_t)n * g.oh * g.ow * g.c;
       Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)n * g.h * g.w * g.c + total) + total);
-      maxpool_fwd_kernel<T><<<grid_for(total), 256, 0, st>>>((const T*)in, g, (T*)l.out, l.arg);
+      maxpool_fwd_kernel<T><<<grid_for(total / 8), 256, 0, st>>>((const T*)in, g, (T*)l.out, l.arg);
     } else {
       const int B = n, K = l.in_units, O = l.out_units;
       long long bps = (long long)cdiv(B, SG_BM) * cdiv(O, SG_BN);
@@ -289,8 +301,8 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         simt_gemm(DenseGT{g, O}, DenseXN<float>{(const float*)x, K}, se, O, K, B, 1, st);
       CE_CHECK_LAUNCH();
       float* bpart = net->ws;
-      colsum_partial_kernel<float><<<dim3(cdiv(O, 256), 1), 256, 0, st>>>(g, B, O, B, bpart);
-      bias_sgd_kernel<<<cdiv(O, 256), 256, 0, st>>>(bpart, 1, O, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
+      int bs = colsum(g, B, O, bpart, st);
+      bias_sgd_kernel<<<cdiv(O, 256), 256, 0, st>>>(bpart, bs, O, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
       CE_CHECK_LAUNCH();
     } else if (l.kind == CE_LAYER_CONV) {
       ConvGeom g = l.g;
@@ -327,10 +339,8 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       CE_CHECK_LAUNCH();
       }
       float* bpart = net->ws + (size_t)splits * g.co * K;
-      int bsplits = std::min(64, std::max(1, Mo / 2048));
-      int mchunk = cdiv(Mo, bsplits);
       Prof pf(net, P_CONV_SGD, 0.0, ab * Mo * g.co + 4.0 * splits * g.co * K + 20.0 * g.co * K, 3);
-      colsum_partial_kernel<T><<<dim3(cdiv(g.co, 128), bsplits), 128, 0, st>>>(dy, Mo, g.co, mchunk, bpart);
+      int bsplits = colsum(dy, Mo, g.co, bpart, st);
       conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(net->ws, splits, g.co, K, g.c, g.k * g.k, l.W, l.VW,
                                                                    keep ? l.GW : nullptr, l.Wbf, l.Wtbf, lr, mu);
       bias_sgd_kernel<<<cdiv(g.co, 256), 256, 0, st>>>(bpart, bsplits, g.co, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
@@ -341,7 +351,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         g.n = n;
         size_t total = (size_t)n * g.h * g.w * g.c;
         Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)n * g.oh * g.ow * g.c * 2 + total));
-        maxpool_bwd_kernel<T, T><<<grid_for(total), 256, 0, st>>>((const T*)gin, l.arg, g, mask, (T*)gout);
+        maxpool_bwd_kernel<T, T><<<grid_for(total / 8), 256, 0, st>>>((const T*)gin, l.arg, g, mask, (T*)gout);
         CE_CHECK_LAUNCH();
       }
     }
@@ -356,10 +366,12 @@ int enqueue_step(ce_net* net, int n, float lr, float mu) {
   int s = enqueue_forward<T>(net, n);
   if (s != CE_OK) return s;
   const Layer& last = net->L.back();
-  Prof pf(net, P_LOSS, 0.0, 16.0 * n * net->classes);
-  xent_kernel<<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes, (float*)net->gbuf[0],
-                                        net->d_losses, net->d_step);
-  CE_CHECK_LAUNCH();
+  {
+    Prof pf(net, P_LOSS, 0.0, 16.0 * n * net->classes);
+    xent_kernel<<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes,
+                                          (float*)net->gbuf[0], net->d_losses, net->d_step);
+    CE_CHECK_LAUNCH();
+  }
   return enqueue_backward<T>(net, n, lr, mu);
 }
 
@@ -512,6 +524,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
   net->in_w = d->in_w;
   net->max_batch = d->max_batch;
   cudaDeviceGetAttribute(&net->num_sms, cudaDevAttrMultiProcessorCount, device);
+  keep_pool_memory(device);
   if (cudaStreamCreateWithFlags(&net->st, cudaStreamNonBlocking) != cudaSuccess) {
     delete net;
     return fail(CE_ECUDA, "stream creation failed");
@@ -612,7 +625,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
       long long bps = (long long)cdiv(B, SG_BM) * cdiv(l.out_units, SG_BN);
       int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms));
       ws = std::max(ws, (size_t)sp * B * l.out_units * 4);
-      ws = std::max(ws, (size_t)l.out_units * 4);
+      ws = std::max(ws, (size_t)(kColsumMaxSplits + 64) * l.out_units * 4);
     } else {
       ALLOC(l.out, B * l.out_per_sample * ab);
       max_g = std::max(max_g, B * l.out_per_sample * ab);
@@ -625,7 +638,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         long long bps = (long long)cdiv(l.g.co, SG_BM) * cdiv(K, SG_BN);
         int sp = simt_splits((int)Mo, pick_splits(bps, Mo, 512, net->num_sms));
         sp = std::max(sp, conv_wgrad_tc_max_splits(l.g, (int)B, net->num_sms));
-        ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)64 * l.g.co * 4);
+        ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);
       }
     }
     if (l.wn) {

@@ -3,6 +3,7 @@
 // dense split-K reduction, softmax cross-entropy, prediction head and the
 // host-layout <-> device-layout parameter permutations.
 #pragma once
+#include <algorithm>
 #include "kernels.cuh"
 
 namespace ce {
@@ -58,63 +59,159 @@ __global__ void nhwc_to_nchw_kernel(const T* __restrict__ x, int B, int C, int C
 }
 
 // ---------------------------------------------------------------- max pool
-// ties -> first window element in row-major order (nn.py:119-150)
+// ties -> first window element in row-major order (nn.py:119-150). One thread
+// per (pixel, 8-channel group): 16-byte loads, 32-bit index math.
+template <class T>
+__device__ __forceinline__ void load8(const T* p, float (&v)[8]);
+template <class T>
+__device__ __forceinline__ void store8(T* p, const float (&v)[8]);
+
 template <class T>
 __global__ void maxpool_fwd_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y, uint8_t* __restrict__ arg) {
-  size_t total = (size_t)g.n * g.oh * g.ow * g.c;
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-    int c = e % g.c;
-    size_t t = e / g.c;
-    int q = t % g.ow;
+  const int cg = g.c / 8;
+  const int total = g.n * g.oh * g.ow * cg;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int c0 = (e % cg) * 8;
+    int t = e / cg;
+    const int q = t % g.ow;
     t /= g.ow;
-    int p = t % g.oh;
-    int n = t / g.oh;
-    const T* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c + c;
-    float best = ldf(base, 0);
-    int bi = 0;
+    const int p = t % g.oh, n = t / g.oh;
+    const T* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c + c0;
+    float best[8];
+    uint8_t bi[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    load8(base, best);
     for (int i = 0; i < g.k; ++i)
       for (int j = 0; j < g.k; ++j) {
-        float v = ldf(base, ((size_t)i * g.w + j) * g.c);
-        if (v > best) {
-          best = v;
-          bi = i * g.k + j;
-        }
+        float v[8];
+        load8(base + ((size_t)i * g.w + j) * g.c, v);
+        const uint8_t idx = (uint8_t)(i * g.k + j);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (v[u] > best[u]) {
+            best[u] = v[u];
+            bi[u] = idx;
+          }
       }
-    stf(y, e, best);
-    if (arg) arg[e] = (uint8_t)bi;
+    const size_t o = (size_t)e * 8;
+    store8(y + o, best);
+    if (arg) *(uint2*)(arg + o) = *(const uint2*)bi;
   }
 }
 
-// gather form: dx[n,h,w,c] = sum over windows (p,q) whose argmax hits (h,w)
+// gather form: dx[n,h,w,c] = sum over windows (p,q) whose argmax hits (h,w),
+// accumulated in window order; optional ReLU mask of the pool input.
 template <class T, class TG>
 __global__ void maxpool_bwd_kernel(const TG* __restrict__ dy, const uint8_t* __restrict__ arg, ConvGeom g,
                                    const T* __restrict__ mask, TG* __restrict__ dx) {
-  size_t total = (size_t)g.n * g.h * g.w * g.c;
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-    int c = e % g.c;
-    size_t t = e / g.c;
-    int wx = t % g.w;
+  const int cg = g.c / 8;
+  const int total = g.n * g.h * g.w * cg;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int c0 = (e % cg) * 8;
+    int t = e / cg;
+    const int wx = t % g.w;
     t /= g.w;
-    int hy = t % g.h;
-    int n = t / g.h;
-    float acc = 0.f;
-    int p_lo = hy - g.k + 1 > 0 ? (hy - g.k + 1 + g.s - 1) / g.s : 0;
-    int p_hi = min(hy / g.s, g.oh - 1);
-    int q_lo = wx - g.k + 1 > 0 ? (wx - g.k + 1 + g.s - 1) / g.s : 0;
-    int q_hi = min(wx / g.s, g.ow - 1);
+    const int hy = t % g.h, n = t / g.h;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int p_lo = hy - g.k + 1 > 0 ? (hy - g.k + 1 + g.s - 1) / g.s : 0;
+    const int p_hi = min(hy / g.s, g.oh - 1);
+    const int q_lo = wx - g.k + 1 > 0 ? (wx - g.k + 1 + g.s - 1) / g.s : 0;
+    const int q_hi = min(wx / g.s, g.ow - 1);
     for (int p = p_lo; p <= p_hi; ++p)
       for (int q = q_lo; q <= q_hi; ++q) {
-        size_t o = (((size_t)n * g.oh + p) * g.ow + q) * g.c + c;
-        int hit = (hy - p * g.s) * g.k + (wx - q * g.s);
-        if (arg[o] == hit) acc += ldf(dy, o);
+        const size_t o = (((size_t)n * g.oh + p) * g.ow + q) * g.c + c0;
+        const uint8_t hit = (uint8_t)((hy - p * g.s) * g.k + (wx - q * g.s));
+        uint2 a2 = *(const uint2*)(arg + o);
+        const uint8_t* a = (const uint8_t*)&a2;
+        float v[8];
+        load8(dy + o, v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (a[u] == hit) acc[u] += v[u];
       }
-    if (mask && !(ldf(mask, e) > 0.f)) acc = 0.f;
-    stf(dx, e, acc);
+    const size_t off = (size_t)e * 8;
+    if (mask) {
+      float m[8];
+      load8(mask + off, m);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (!(m[u] > 0.f)) acc[u] = 0.f;
+    }
+    store8(dx + off, acc);
   }
 }
 
 // ---------------------------------------------------------------- reductions
-// part[split][o] = sum_{m in split} dy[m][o]
+// Column sums of a row-major [M][N] matrix (bias gradients):
+// part[block][o] = sum over the block's rows of dy[m][o]. Each thread owns 8
+// consecutive columns (one 16-byte bf16 load / two float4), a block covers
+// 256/(N/8) rows per iteration, and the block's row-groups are reduced in
+// shared memory in a fixed order (deterministic).
+template <class T>
+__device__ __forceinline__ void load8(const T* p, float (&v)[8]);
+template <>
+__device__ __forceinline__ void load8<bf16>(const bf16* p, float (&v)[8]) {
+  uint4 u = *(const uint4*)p;
+  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
+  float4 a = *(const float4*)p, b = *(const float4*)(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <class T>
+__device__ __forceinline__ void store8(T* p, const float (&v)[8]);
+template <>
+__device__ __forceinline__ void store8<bf16>(bf16* p, const float (&v)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = (__nv_bfloat162*)&u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *(uint4*)p = u;
+}
+template <>
+__device__ __forceinline__ void store8<float>(float* p, const float (&v)[8]) {
+  *(float4*)p = make_float4(v[0], v[1], v[2], v[3]);
+  *(float4*)(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) colsum8_kernel(const T* __restrict__ dy, int M, int N, int rows_per_block,
+                                                      float* __restrict__ part) {
+  __shared__ float red[256][9];
+  const int groups = N / 8;                 // column groups (N % 8 == 0)
+  const int rgroups = 256 / groups;         // rows processed per iteration
+  const int cg = threadIdx.x % groups, rg = threadIdx.x / groups;
+  const int m0 = blockIdx.x * rows_per_block, m1 = min(M, m0 + rows_per_block);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (rg < rgroups) {
+    for (int m = m0 + rg; m < m1; m += rgroups) {
+      float v[8];
+      load8(dy + (size_t)m * N + cg * 8, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[threadIdx.x][i] = acc[i];
+  __syncthreads();
+  if (threadIdx.x < groups) {
+    float tot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < rgroups; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) tot[i] += red[r * groups + threadIdx.x][i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) part[(size_t)blockIdx.x * N + threadIdx.x * 8 + i] = tot[i];
+  }
+}
+
+// generic (any N) fallback for dense biases with N % 8 != 0
 template <class T>
 __global__ void colsum_partial_kernel(const T* __restrict__ dy, int M, int N, int mchunk, float* __restrict__ part) {
   const int split = blockIdx.y;
@@ -124,6 +221,22 @@ __global__ void colsum_partial_kernel(const T* __restrict__ dy, int M, int N, in
     for (int m = m0; m < m1; ++m) acc += ldf(dy, (size_t)m * N + o);
     part[(size_t)split * N + o] = acc;
   }
+}
+
+constexpr int kColsumMaxSplits = 512;
+
+// launches the column sum; returns the number of partial rows written
+template <class T>
+inline int colsum(const T* dy, int M, int N, float* part, cudaStream_t st) {
+  if (N % 8 == 0 && N <= 2048) {
+    int rows = std::max(64, cdiv(M, kColsumMaxSplits));
+    int blocks = cdiv(M, rows);
+    colsum8_kernel<T><<<blocks, 256, 0, st>>>(dy, M, N, rows, part);
+    return blocks;
+  }
+  int splits = std::max(1, std::min(64, M / 64));
+  colsum_partial_kernel<T><<<dim3(cdiv(N, 128), splits), 128, 0, st>>>(dy, M, N, cdiv(M, splits), part);
+  return splits;
 }
 
 // conv weights: g = sum_split part[split][o][kk]; momentum update of W (fp32 master)
