@@ -26,40 +26,44 @@ inline bool conv_tc_enabled() {
 }
 
 // ------------------------------------------------------------------ forward
+// table: xoff[k8] = im2col offset of K chunk k8 = (tap, c0) relative to the
+// output pixel's receptive-field origin: (i*W + j)*C + c0.
 struct FwdTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
   const bf16* x;
   const bf16* w;  // [o][K]
   ConvGeom g;
   int K, M, BN;
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid) const {
-    // A: this thread owns row r = ptid of the tile (128 rows, 128 producers)
+  FastDiv d_ow, d_oh;
+  __device__ void init(uint8_t* table, int tid, int nthreads) const {
+    int* xoff = (int*)table;
+    for (int k8 = tid; k8 < K / 8; k8 += nthreads) {
+      const int kk = k8 * 8, tap = kk / g.c, c0 = kk - tap * g.c;
+      const int i = tap / g.k, j = tap - i * g.k;
+      xoff[k8] = (i * g.w + j) * g.c + c0;
+    }
+  }
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table) const {
+    const int* xoff = (const int*)table;
     {
-      const int r = ptid;
+      const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;  // 256 producers: 2 threads per row
       const int m = c.m0 + r;
       const bool row_ok = m < M;
-      int q = 0, p = 0, n = 0;
+      uint32_t q = 0, p = 0, n = 0, t = 0;
       if (row_ok) {
-        q = m % g.ow;
-        int t = m / g.ow;
-        p = t % g.oh;
-        n = t / g.oh;
+        d_ow.divmod((uint32_t)m, t, q);
+        d_oh.divmod(t, n, p);
       }
       const bf16* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
 #pragma unroll
-      for (int kc = 0; kc < 8; ++kc) {
-        const int kk = kb * TC_BK + kc * 8;
-        const bool ok = row_ok && kk < K;
-        const bf16* src = x;
-        if (ok) {
-          const int tap = kk / g.c, c0 = kk - tap * g.c;
-          const int i = tap / g.k, j = tap - i * g.k;
-          src = base + ((size_t)i * g.w + j) * g.c + c0;
-        }
-        cp_async16(sA + kmajor_off(TC_BM, r, kc), src, ok ? 16u : 0u);
+      for (int e = 0; e < 4; ++e) {
+        const int kc = kc0 + 2 * e;
+        const int k8 = kb * 8 + kc;
+        const bool ok = row_ok && k8 * 8 < K;
+        cp_async16(sA + kmajor_off(TC_BM, r, kc), ok ? (const void*)(base + xoff[k8]) : (const void*)x,
+                   ok ? 16u : 0u);
       }
     }
-    // B: weights, BN rows x 8 chunks
     for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
       const int r = ch % BN, kc = ch / BN;
       const int o = c.n0 + r, kk = kb * TC_BK + kc * 8;
@@ -82,7 +86,7 @@ struct FwdTcEpi {
     __align__(16) bf16 out[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float t = v[i] + (o0 + i < co ? bias[o0 + i] : 0.f);
+      float t = v[i] + (o0 + i < co ? __ldg(bias + o0 + i) : 0.f);
       if (relu) t = t > 0.f ? t : 0.f;
       out[i] = __float2bfloat16_rn(t);
     }
@@ -97,6 +101,7 @@ struct FwdTcEpi {
 // residue class (rh, rw) only receive taps i = rh + s*a, j = rw + s*b, from
 // dy[n, hh - a, ww - b]; each class is a dense stride-1 implicit GEMM with
 // K = ti*tj*C_out, so no MMA work is spent on off-lattice taps.
+// table per K chunk k8 = (a, b, o0): dy offset delta, packed (a, b), Wt offset.
 struct DgradClass {
   int rh, rw;   // residue class
   int ti, tj;   // valid taps per axis
@@ -110,45 +115,56 @@ struct DgradTcLoader {
   ConvGeom g;
   DgradClass cl;
   int K, M, BN;    // K = ti*tj*co, M = n*hc*wc
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid) const {
+  FastDiv d_wc, d_hc;
+  __device__ void init(uint8_t* table, int tid, int nthreads) const {
+    const int nk8 = K / 8;
+    int* doff = (int*)table;
+    int* dab = doff + nk8;
+    int* woff = dab + nk8;
+    for (int k8 = tid; k8 < nk8; k8 += nthreads) {
+      const int kk = k8 * 8, tap = kk / g.co, o0 = kk - tap * g.co;
+      const int a = tap / cl.tj, b = tap - a * cl.tj;
+      const int i = cl.rh + g.s * a, j = cl.rw + g.s * b;
+      doff[k8] = o0 - (a * g.ow + b) * g.co;
+      dab[k8] = (a << 16) | b;
+      woff[k8] = (i * g.k + j) * g.co + o0;
+    }
+  }
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table) const {
+    const int nk8 = K / 8;
+    const int* doff = (const int*)table;
+    const int* dab = doff + nk8;
+    const int* woff = dab + nk8;
     {
-      const int r = ptid;
+      const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;
       const int m = c.m0 + r;
       const bool row_ok = m < M;
-      int ww = 0, hh = 0, n = 0;
+      uint32_t ww = 0, hh = 0, n = 0, t = 0;
       if (row_ok) {
-        ww = m % cl.wc;
-        int t = m / cl.wc;
-        hh = t % cl.hc;
-        n = t / cl.hc;
+        d_wc.divmod((uint32_t)m, t, ww);
+        d_hc.divmod(t, n, hh);
       }
       const bf16* row = dy + (((size_t)n * g.oh + hh) * g.ow + ww) * g.co;
 #pragma unroll
-      for (int kc = 0; kc < 8; ++kc) {
-        const int kk = kb * TC_BK + kc * 8;
-        bool ok = row_ok && kk < K;
+      for (int e = 0; e < 4; ++e) {
+        const int kc = kc0 + 2 * e;
+        const int k8 = kb * 8 + kc;
+        bool ok = row_ok && k8 < nk8;
         const bf16* src = dy;
         if (ok) {
-          const int tap = kk / g.co, o0 = kk - tap * g.co;
-          const int a = tap / cl.tj, b = tap - a * cl.tj;
-          ok = hh >= a && ww >= b && hh - a < g.oh && ww - b < g.ow;
-          if (ok) src = row - ((size_t)a * g.ow + b) * g.co + o0;
+          const int ab = dab[k8], a = ab >> 16, b = ab & 0xFFFF;
+          ok = (int)hh >= a && (int)ww >= b && (int)hh - a < g.oh && (int)ww - b < g.ow;
+          if (ok) src = row + doff[k8];
         }
         cp_async16(sA + kmajor_off(TC_BM, r, kc), src, ok ? 16u : 0u);
       }
     }
     for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
       const int r = ch % BN, kc = ch / BN;
-      const int cc = c.n0 + r, kk = kb * TC_BK + kc * 8;
-      const bool ok = cc < g.c && kk < K;
-      const bf16* src = wt;
-      if (ok) {
-        const int tap = kk / g.co, o0 = kk - tap * g.co;
-        const int a = tap / cl.tj, b = tap - a * cl.tj;
-        const int i = cl.rh + g.s * a, j = cl.rw + g.s * b;
-        src = wt + ((size_t)cc * g.k * g.k + i * g.k + j) * g.co + o0;
-      }
-      cp_async16(sB + kmajor_off(BN, r, kc), src, ok ? 16u : 0u);
+      const int cc = c.n0 + r, k8 = kb * 8 + kc;
+      const bool ok = cc < g.c && k8 < nk8;
+      cp_async16(sB + kmajor_off(BN, r, kc),
+                 ok ? (const void*)(wt + (size_t)cc * g.k * g.k * g.co + woff[k8]) : (const void*)wt, ok ? 16u : 0u);
     }
   }
 };
@@ -159,13 +175,14 @@ struct DgradTcEpi {
   ConvGeom g;
   DgradClass cl;
   int M;
+  FastDiv d_wc, d_hc;
   __device__ void store(const TileCoord& tc, int row, int col, const float (&v)[16]) const {
     const int m = tc.m0 + row;
     const int c0 = tc.n0 + col;
     if (m >= M || c0 >= g.c) return;
-    const int ww = m % cl.wc;
-    const int t = m / cl.wc;
-    const int hh = t % cl.hc, n = t / cl.hc;
+    uint32_t ww, hh, n, t;
+    d_wc.divmod((uint32_t)m, t, ww);
+    d_hc.divmod(t, n, hh);
     const size_t off = (((size_t)n * g.h + cl.rh + g.s * hh) * g.w + cl.rw + g.s * ww) * g.c + c0;
     __align__(16) bf16 out[16];
     __align__(16) bf16 mk[16];
@@ -194,8 +211,10 @@ struct WgradTcLoader {
   int Kf;  // k*k*c (rows of D)
   int Mo;  // reduction length n*oh*ow
   int BN;
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid) const {
-    // A: 16 groups of 8 (i,j,c) rows x 64 reduction indices
+  FastDiv d_ow, d_oh;
+  __device__ void init(uint8_t*, int, int) const {}
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*) const {
+    // A: 16 groups of 8 (i,j,c) rows x 64 reduction indices; 256 producers -> 4 chunks each
     {
       const int grp = ptid & 15;
       const int kk0 = c.m0 + grp * 8;
@@ -207,15 +226,15 @@ struct WgradTcLoader {
         tap_off = (i * g.w + j) * g.c + c0;
       }
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int kr = (ptid >> 4) + e * 8;  // 0..63
+      for (int e = 0; e < 4; ++e) {
+        const int kr = (ptid >> 4) + e * 16;  // 0..63
         const int m = kb * TC_BK + kr;
         const bool ok = grp_ok && m < Mo;
         const bf16* src = x;
         if (ok) {
-          const int q = m % g.ow;
-          const int t = m / g.ow;
-          const int p = t % g.oh, n = t / g.oh;
+          uint32_t t, q, p, n;
+          d_ow.divmod((uint32_t)m, t, q);
+          d_oh.divmod(t, n, p);
           src = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c + tap_off;
         }
         cp_async16(sA + mnmajor_off(TC_BM, grp, kr), src, ok ? 16u : 0u);
@@ -262,10 +281,11 @@ inline int with_bn(int n, Fn&& fn) {
 inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const float* bias, int relu, bf16* y,
                        int num_sms, cudaStream_t st) {
   const int M = g.n * g.oh * g.ow, K = g.k * g.k * g.c;
+  if ((K / 8) * 4 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_fwd_tc: K=%d exceeds the chunk table", K);
   return with_bn(g.co, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
-    FwdTcLoader ld{x, w, g, K, M, BN};
+    FwdTcLoader ld{x, w, g, K, M, BN, FastDiv(g.ow), FastDiv(g.oh)};
     FwdTcEpi ep{y, bias, M, g.co, relu};
     cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc: %s", cudaGetErrorString(e));
@@ -293,11 +313,12 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
       cl.wc = (g.w - rw + g.s - 1) / g.s;
       if (cl.ti == 0 || cl.tj == 0) continue;
       const int M = g.n * cl.hc * cl.wc, K = cl.ti * cl.tj * g.co;
+      if ((K / 8) * 12 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_dgrad_tc: K=%d exceeds the chunk table", K);
       int s = with_bn(g.c, [&](auto bn) {
         constexpr int BN = decltype(bn)::value;
         TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
-        DgradTcLoader ld{dy, wt, g, cl, K, M, BN};
-        DgradTcEpi ep{dx, mask, g, cl, M};
+        DgradTcLoader ld{dy, wt, g, cl, K, M, BN, FastDiv(cl.wc), FastDiv(cl.hc)};
+        DgradTcEpi ep{dx, mask, g, cl, M, FastDiv(cl.wc), FastDiv(cl.hc)};
         cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
         return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_dgrad_tc: %s", cudaGetErrorString(e));
       });
@@ -327,7 +348,7 @@ inline int conv_wgrad_tc(const ConvGeom& g, const bf16* x, const bf16* dy, float
     constexpr int BN = decltype(bn)::value;
     TcShape sh = tc_make_shape(Kf, g.co, Mo, BN, want);
     *splits_out = sh.splits;
-    WgradTcLoader ld{x, dy, g, Kf, Mo, BN};
+    WgradTcLoader ld{x, dy, g, Kf, Mo, BN, FastDiv(g.ow), FastDiv(g.oh)};
     WgradTcEpi ep{part, Kf, g.co};
     cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_wgrad_tc: %s", cudaGetErrorString(e));

@@ -7,9 +7,13 @@
 // (zero-fill for padding / invalid taps), and an Epilogue policy consumes the
 // fp32 accumulator rows. Roles per CTA (persistent, grid <= #SMs):
 //
-//   warps 0-3  producers: cp.async gather into an S-stage smem ring
-//   warps 4-7  epilogue : tcgen05.ld TMEM -> registers -> Epilogue::store
-//   warp  8    MMA      : TMEM alloc + one elected thread issuing tcgen05.mma
+//   warps 0-7   producers: cp.async gather into an S-stage smem ring
+//   warps 8-11  epilogue : tcgen05.ld TMEM -> registers -> Epilogue::store
+//   warp  12    MMA      : TMEM alloc + one elected thread issuing tcgen05.mma
+//
+// Before the role split every thread helps the Loader fill a small shared
+// table (Loader::init), e.g. the im2col offset of every 16-byte K chunk, so the
+// producers' inner loop is a table lookup instead of runtime divisions.
 //
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile t overlap the
 // MMAs of tile t+1. Shared-memory tiles use the SWIZZLE_NONE canonical layouts
@@ -22,9 +26,31 @@ namespace ce {
 
 constexpr int TC_BM = 128;  // UMMA M (rows per tile = TMEM lanes)
 constexpr int TC_BK = 64;   // K elements per pipeline stage (8 x 16-byte chunks)
-constexpr int TC_PRODUCERS = 128;
-constexpr int TC_THREADS = 288;
-constexpr int TC_LAG = 2;  // cp.async groups kept in flight before signalling
+constexpr int TC_PRODUCERS = 256;
+constexpr int TC_EPI_WARP0 = TC_PRODUCERS / 32;   // first epilogue warp (8)
+constexpr int TC_MMA_WARP = TC_EPI_WARP0 + 4;      // 12
+constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 416
+constexpr int TC_TABLE_BYTES = 20480;              // loader lookup tables
+constexpr int TC_MAX_LAG = 8;
+
+// Division by a runtime-invariant divisor d (1 <= d < 2^31) for 0 <= n < 2^31:
+// q = (n * M) >> (32 + l), M = ceil(2^(32+l) / d), l = ceil(log2 d).
+struct FastDiv {
+  uint64_t mul;
+  uint32_t shift, d;
+  FastDiv() = default;
+  __host__ __device__ explicit FastDiv(uint32_t div) : d(div) {
+    uint32_t l = 0;
+    while ((1ull << l) < div) ++l;
+    shift = 32 + l;
+    mul = ((1ull << shift) + div - 1) / div;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (uint32_t)(((uint64_t)n * mul) >> shift); }
+  __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
+    q = div(n);
+    r = n - q * d;
+  }
+};
 
 // Tile coordinates handed to loaders / epilogues.
 struct TileCoord {
@@ -79,10 +105,11 @@ struct TcSmemLayout {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
+  static constexpr int STAGES = (196 * 1024 / STAGE_BYTES) > 8 ? 8 : (196 * 1024 / STAGE_BYTES);
+  static constexpr int LAG = STAGES - 1 > TC_MAX_LAG ? TC_MAX_LAG : STAGES - 1;  // cp.async groups in flight
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + alignment slack
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + TC_TABLE_BYTES + BAR_BYTES + 1024;  // + alignment slack
 };
 
 template <int BN, class Loader, class Epi>
@@ -92,7 +119,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + S * L::STAGE_BYTES);
+  uint8_t* table = smem + S * L::STAGE_BYTES;
+  uint64_t* full = (uint64_t*)(table + TC_TABLE_BYTES);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -113,19 +141,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 8) tmem_alloc(tmem_base_slot, L::TMEM_COLS);
+  if (warp == TC_MMA_WARP) tmem_alloc(tmem_base_slot, L::TMEM_COLS);
+  ld.init(table, threadIdx.x, TC_THREADS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   const uint32_t smem_base = smem_u32(smem);
 
-  if (warp < 4) {
+  if (warp < TC_EPI_WARP0) {
     // ------------------------------------------------------------ producers
+    constexpr int LAG = L::LAG;
     const int ptid = threadIdx.x;
     int stage = 0;
     uint32_t phase = 0;
-    int pending_stage[TC_LAG + 1];
+    int pending_stage[TC_MAX_LAG + 1];
     int npending = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
       TileCoord c = tc_tile(shape, t, BN);
@@ -133,14 +163,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
         const uint32_t sB = sA + L::A_BYTES;
-        ld.load(c, c.kb0 + kb, sA, sB, ptid);
+        ld.load(c, c.kb0 + kb, sA, sB, ptid, table);
         cp_async_commit();
-        // retire the oldest group once TC_LAG newer ones are in flight
-        if (npending == TC_LAG) {
-          cp_async_wait<TC_LAG>();
+        // retire the oldest group once LAG newer ones are in flight
+        if (npending == LAG) {
+          cp_async_wait<LAG>();
           fence_proxy_async();
           mbar_arrive(&full[pending_stage[0]]);
-          for (int i = 0; i < TC_LAG - 1; ++i) pending_stage[i] = pending_stage[i + 1];
+#pragma unroll
+          for (int i = 0; i < LAG - 1; ++i) pending_stage[i] = pending_stage[i + 1];
           --npending;
         }
         pending_stage[npending++] = stage;
@@ -153,9 +184,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     cp_async_wait_all();
     fence_proxy_async();
     for (int i = 0; i < npending; ++i) mbar_arrive(&full[pending_stage[i]]);
-  } else if (warp < 8) {
+  } else if (warp < TC_MMA_WARP) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp - 4;  // TMEM lane quarter (warp % 4 == q)
+    const int q = warp & 3;  // TMEM lane quarter (warp % 4 == q)
     const int row_in_tile = q * 32 + lane;
     int lt = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++lt) {
@@ -221,7 +252,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == TC_MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem_base, L::TMEM_COLS);
   }
