@@ -15,6 +15,8 @@
 //          (nn.py:108-115, 306-322)
 #pragma once
 #include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "tc_engine.cuh"
 #include "kernels.cuh"
 
@@ -25,11 +27,39 @@ inline bool conv_tc_enabled() {
   return !(e && e[0] == '1');
 }
 
+// TMA descriptor for a K-major bf16 operand [rows][K] (K contiguous, K % 8 == 0):
+// box = 64 K-elements (128 B, SWIZZLE_128B) x `box_rows` rows; OOB reads are zeros.
+inline bool make_tmap_kmajor(CUtensorMap* map, const bf16* base, int rows, int K, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+inline bool tma_disabled() {
+  const char* e = getenv("CE_DISABLE_TMA");
+  return e && e[0] == '1';
+}
+
 // ------------------------------------------------------------------ forward
 // table: xoff[k8] = im2col offset of K chunk k8 = (tap, c0) relative to the
 // output pixel's receptive-field origin: (i*W + j)*C + c0.
+template <bool TMA_B>
 struct FwdTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  static constexpr bool B_TMA_SW128 = TMA_B;
+  CUtensorMap wmap;  // B operand (weights) when TMA_B
   const bf16* x;
   const bf16* w;  // [o][K]
   ConvGeom g;
@@ -43,8 +73,15 @@ struct FwdTcLoader {
       xoff[k8] = (i * g.w + j) * g.c + c0;
     }
   }
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table) const {
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
+                       uint64_t* full) const {
     const int* xoff = (const int*)table;
+    if (TMA_B) {
+      if (ptid == 0) {
+        mbar_expect_tx(full, (uint32_t)BN * 128u);
+        tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+      }
+    }
     {
       const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;  // 256 producers: 2 threads per row
       const int m = c.m0 + r;
@@ -64,12 +101,14 @@ struct FwdTcLoader {
                    ok ? 16u : 0u);
       }
     }
-    for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
-      const int r = ch % BN, kc = ch / BN;
-      const int o = c.n0 + r, kk = kb * TC_BK + kc * 8;
-      const bool ok = o < g.co && kk < K;
-      cp_async16(sB + kmajor_off(BN, r, kc), ok ? (const void*)(w + (size_t)o * K + kk) : (const void*)w,
-                 ok ? 16u : 0u);
+    if (!TMA_B) {
+      for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
+        const int r = ch % BN, kc = ch / BN;
+        const int o = c.n0 + r, kk = kb * TC_BK + kc * 8;
+        const bool ok = o < g.co && kk < K;
+        cp_async16(sB + kmajor_off(BN, r, kc), ok ? (const void*)(w + (size_t)o * K + kk) : (const void*)w,
+                   ok ? 16u : 0u);
+      }
     }
   }
 };
@@ -110,6 +149,7 @@ struct DgradClass {
 
 struct DgradTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  static constexpr bool B_TMA_SW128 = false;
   const bf16* dy;
   const bf16* wt;  // [c][k*k][co]
   ConvGeom g;
@@ -130,7 +170,8 @@ struct DgradTcLoader {
       woff[k8] = (i * g.k + j) * g.co + o0;
     }
   }
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table) const {
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
+                       uint64_t*) const {
     const int nk8 = K / 8;
     const int* doff = (const int*)table;
     const int* dab = doff + nk8;
@@ -205,6 +246,7 @@ struct DgradTcEpi {
 // ------------------------------------------------------------------ wgrad
 struct WgradTcLoader {
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
+  static constexpr bool B_TMA_SW128 = false;
   const bf16* x;
   const bf16* dy;
   ConvGeom g;
@@ -213,7 +255,8 @@ struct WgradTcLoader {
   int BN;
   FastDiv d_ow, d_oh;
   __device__ void init(uint8_t*, int, int) const {}
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*) const {
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
+                       uint64_t*) const {
     // A: 16 groups of 8 (i,j,c) rows x 64 reduction indices; 256 producers -> 4 chunks each
     {
       const int grp = ptid & 15;
@@ -285,9 +328,19 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
   return with_bn(g.co, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
-    FwdTcLoader ld{x, w, g, K, M, BN, FastDiv(g.ow), FastDiv(g.oh)};
     FwdTcEpi ep{y, bias, M, g.co, relu};
-    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    cudaError_t e;
+    FwdTcLoader<true> ldt{};
+    if (!tma_disabled() && make_tmap_kmajor(&ldt.wmap, w, g.co, K, BN)) {
+      ldt.x = x; ldt.w = w; ldt.g = g; ldt.K = K; ldt.M = M; ldt.BN = BN;
+      ldt.d_ow = FastDiv(g.ow); ldt.d_oh = FastDiv(g.oh);
+      e = tc_launch<BN>(ldt, ep, sh, num_sms, st);
+    } else {
+      FwdTcLoader<false> ld{};
+      ld.x = x; ld.w = w; ld.g = g; ld.K = K; ld.M = M; ld.BN = BN;
+      ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    }
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc: %s", cudaGetErrorString(e));
   });
 }

@@ -15,12 +15,14 @@ template <int AMN, int BMN>
 struct PlainLoader {
   static constexpr int A_MN_MAJOR = AMN;
   static constexpr int B_MN_MAJOR = BMN;
+  static constexpr bool B_TMA_SW128 = false;
   const __nv_bfloat16* A;
   const __nv_bfloat16* B;
   int M, N, K;
   int BN;
   __device__ void init(uint8_t*, int, int) const {}
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*) const {
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
+                       uint64_t*) const {
     const int k0 = kb * TC_BK;
     // A tile: 128 rows x 64 k = 1024 chunks
     for (int ch = ptid; ch < TC_BM * 8; ch += TC_PRODUCERS) {
