@@ -29,7 +29,8 @@ inline bool conv_tc_enabled() {
 
 // TMA descriptor for a K-major bf16 operand [rows][K] (K contiguous, K % 8 == 0):
 // box = 64 K-elements (128 B, SWIZZLE_128B) x `box_rows` rows; OOB reads are zeros.
-inline bool make_tmap_kmajor(CUtensorMap* map, const bf16* base, int rows, int K, int box_rows) {
+inline bool make_tmap_kmajor(CUtensorMap* map, const bf16* base, int rows, int K, int box_rows, int row_stride = 0) {
+  if (row_stride <= 0) row_stride = K;
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -38,7 +39,7 @@ inline bool make_tmap_kmajor(CUtensorMap* map, const bf16* base, int rows, int K
       return false;
   }
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint64_t strides[1] = {(cuuint64_t)row_stride * 2};
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)base, dims, strides, box, estr,
@@ -58,7 +59,7 @@ inline bool tma_disabled() {
 template <bool TMA_B>
 struct FwdTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool B_TMA_SW128 = TMA_B;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B;
   CUtensorMap wmap;  // B operand (weights) when TMA_B
   const bf16* x;
   const bf16* w;  // [o][K]
@@ -149,7 +150,7 @@ struct DgradClass {
 
 struct DgradTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool B_TMA_SW128 = false;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false;
   const bf16* dy;
   const bf16* wt;  // [c][k*k][co]
   ConvGeom g;
@@ -246,7 +247,7 @@ struct DgradTcEpi {
 // ------------------------------------------------------------------ wgrad
 struct WgradTcLoader {
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
-  static constexpr bool B_TMA_SW128 = false;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false;
   const bf16* x;
   const bf16* dy;
   ConvGeom g;

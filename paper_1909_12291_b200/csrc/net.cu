@@ -15,6 +15,7 @@
 #include <atomic>
 #include "ops.cuh"
 #include "conv_tc.cuh"
+#include "dense_tc.cuh"
 
 namespace ce {
 
@@ -46,6 +47,9 @@ struct Layer {
   int pidx = -1;
   float *W = nullptr, *b = nullptr, *VW = nullptr, *Vb = nullptr, *GW = nullptr, *Gb = nullptr;
   bf16 *Wbf = nullptr, *Wtbf = nullptr;
+  bf16* Wbp = nullptr;    // dense: bf16 mirror [out][in_pad]
+  bf16* x16 = nullptr;    // dense after dense: bf16 copy of the fp32 input [B][in_pad]
+  int in_pad = 0, out_pad = 0;
   size_t wn = 0;
   int bn = 0;
   void* out = nullptr;
@@ -95,6 +99,7 @@ struct ce_net {
   void* x0 = nullptr;
   int32_t* ybatch = nullptr;
   void* gbuf[2] = {nullptr, nullptr};
+  bf16* gbf = nullptr;  // bf16 copy of a dense output gradient [B][out_pad]
   size_t gbytes = 0;
   float* ws = nullptr;
   size_t ws_bytes = 0;
@@ -242,11 +247,23 @@ int enqueue_forward(ce_net* net, int n) {
       long long bps = (long long)cdiv(B, SG_BM) * cdiv(O, SG_BN);
       int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms));
       Prof pf(net, P_DENSE_FWD, 2.0 * B * K * O, 4.0 * K * O + (in_act ? act_bytes(net) : 4.0) * B * K, 2);
-      PartialEpi pe{net->ws, B, O};
-      if (in_act)
-        simt_gemm(DenseXA<T>{(const T*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
-      else
-        simt_gemm(DenseXA<float>{(const float*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
+      if (net->use_tc) {
+        const bf16* x16 = (const bf16*)in;
+        if (!in_act) {
+          f32_to_bf16_pad_kernel<<<grid_for((size_t)B * l.in_pad), 256, 0, st>>>((const float*)in, B, K, l.in_pad,
+                                                                                   l.x16);
+          x16 = l.x16;
+          net->acc += 1;
+        }
+        int s = dense_fwd_tc(x16, l.in_pad, l.Wbp, K, l.in_pad, O, B, net->ws, &splits, net->num_sms, st);
+        if (s != CE_OK) return s;
+      } else {
+        PartialEpi pe{net->ws, B, O};
+        if (in_act)
+          simt_gemm(DenseXA<T>{(const T*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
+        else
+          simt_gemm(DenseXA<float>{(const float*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
+      }
       dense_reduce_kernel<<<grid_for((size_t)B * O), 256, 0, st>>>(net->ws, splits, B, O, l.b, (float*)l.out);
     }
     CE_CHECK_LAUNCH();
@@ -286,6 +303,21 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       Prof pf(net, P_DENSE_BWD, (l.need_dx ? 4.0 : 2.0) * B * K * O,
               (l.need_dx ? 24.0 : 20.0) * K * O + 2.0 * (l.in_is_act ? act_bytes(net) : 4.0) * B * K,
               l.need_dx ? 4 : 3);
+      if (net->use_tc) {
+        f32_to_bf16_pad_kernel<<<grid_for((size_t)B * l.out_pad), 256, 0, st>>>(g, B, O, l.out_pad, net->gbf);
+        CE_CHECK_LAUNCH();
+        if (l.need_dx) {
+          int s = l.in_is_act ? dense_dx_tc(l.Wbp, net->gbf, K, l.in_pad, O, l.out_pad, B, mask, (T*)gout,
+                                            net->num_sms, st)
+                              : dense_dx_tc(l.Wbp, net->gbf, K, l.in_pad, O, l.out_pad, B, (const float*)nullptr,
+                                            (float*)gout, net->num_sms, st);
+          if (s != CE_OK) return s;
+        }
+        const bf16* xb = l.in_is_act ? (const bf16*)x : l.x16;
+        int s = dense_dw_sgd_tc(xb, l.in_pad, net->gbf, K, l.in_pad, O, l.out_pad, B, l.W, l.VW, keep ? l.GW : nullptr,
+                                l.Wbp, lr, mu, net->num_sms, st);
+        if (s != CE_OK) return s;
+      } else {
       if (l.need_dx) {
         if (l.in_is_act)
           simt_gemm(DenseGA{g, O}, DenseWN{l.W, K}, DenseDxEpi<T, T>{(T*)gout, mask, K}, B, K, O, 1, st);
@@ -300,6 +332,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       else
         simt_gemm(DenseGT{g, O}, DenseXN<float>{(const float*)x, K}, se, O, K, B, 1, st);
       CE_CHECK_LAUNCH();
+      }
       float* bpart = net->ws;
       int bs = colsum(g, B, O, bpart, st);
       bias_sgd_kernel<<<cdiv(O, 256), 256, 0, st>>>(bpart, bs, O, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
@@ -613,7 +646,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
     if (l.kind == CE_LAYER_DENSE) total_params += (size_t)l.out_units * l.in_units;
   }
   net->keep_grads = total_params <= (64u << 20);
-  size_t max_g = (size_t)B * net->in_cp * net->in_h * net->in_w * ab, ws = 0;
+  size_t max_g = (size_t)B * net->in_cp * net->in_h * net->in_w * ab, ws = 0, gbf_elems = 0;
   for (size_t i = 0; i < net->L.size(); ++i) {
     Layer& l = net->L[i];
     if (l.kind == CE_LAYER_DENSE) {
@@ -622,6 +655,16 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
       max_g = std::max(max_g, B * (size_t)l.in_units * (l.in_is_act ? ab : 4));
       l.wn = (size_t)l.out_units * l.in_units;
       l.bn = l.out_units;
+      l.in_pad = (l.in_units + 7) / 8 * 8;
+      l.out_pad = (l.out_units + 7) / 8 * 8;
+      if (net->use_tc) {
+        if (l.in_is_act && l.in_pad != l.in_units) return bail(fail(CE_EINVAL, "feature width not a multiple of 8"));
+        ALLOC(l.Wbp, (size_t)l.out_units * l.in_pad * 2);
+        if (!l.in_is_act) ALLOC(l.x16, B * (size_t)l.in_pad * 2);
+        gbf_elems = std::max(gbf_elems, B * (size_t)l.out_pad);
+        int spt = dense_fwd_splits(l.out_units, l.in_units, net->num_sms);
+        ws = std::max(ws, (size_t)spt * B * l.out_units * 4);
+      }
       long long bps = (long long)cdiv(B, SG_BM) * cdiv(l.out_units, SG_BN);
       int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms));
       ws = std::max(ws, (size_t)sp * B * l.out_units * 4);
@@ -669,6 +712,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
   net->gbytes = max_g;
   ALLOC(net->ws, ws);
   net->ws_bytes = ws;
+  if (gbf_elems) ALLOC(net->gbf, gbf_elems * 2);
   ALLOC(net->d_step, 16);
   net->losses_cap = 4096;
   ALLOC(net->d_losses, net->losses_cap * 4);
@@ -735,6 +779,9 @@ int ce_net_set_params(ce_net* net, int p, const float* w, const float* b) {
   CE_CUDA(cudaMemsetAsync(l.VW, 0, l.wn * 4, st));
   CE_CUDA(cudaMemsetAsync(l.Vb, 0, l.bn * 4, st));
   if (l.Wbf) f32_to_bf16_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.wn, l.Wbf);
+  if (l.Wbp)
+    f32_to_bf16_pad_kernel<<<grid_for((size_t)l.out_units * l.in_pad), 256, 0, st>>>(l.W, l.out_units, l.in_units,
+                                                                                      l.in_pad, l.Wbp);
   if (l.Wtbf) conv_wt_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.g.co, l.g.k * l.g.k, l.g.c, l.Wtbf);
   CE_CHECK_LAUNCH();
   CE_CUDA(cudaStreamSynchronize(st));

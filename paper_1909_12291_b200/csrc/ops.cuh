@@ -397,6 +397,17 @@ __global__ void dense_w_to_host_kernel(const float* __restrict__ w, size_t rows,
     hw[e] = w[r * in_dev + px * cp + ch];
   }
 }
+// [rows][cols] fp32 -> [rows][cols_pad] bf16 with zero padding
+__global__ void f32_to_bf16_pad_kernel(const float* __restrict__ a, size_t rows, int cols, int cols_pad,
+                                       bf16* __restrict__ b) {
+  size_t total = rows * cols_pad;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    size_t r = e / cols_pad;
+    int c = e % cols_pad;
+    b[e] = c < cols ? __float2bfloat16_rn(a[r * cols + c]) : __float2bfloat16_rn(0.f);
+  }
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ a, size_t n, bf16* __restrict__ b) {
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     b[e] = __float2bfloat16_rn(a[e]);

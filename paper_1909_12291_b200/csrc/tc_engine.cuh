@@ -235,7 +235,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < nk16; ++k) {
             // K-major: a K=16 step covers chunks 2k, 2k+1 (LBO apart).
             // MN-major: a K=16 step covers K groups 2k, 2k+1 (LBO apart).
-            const uint64_t ad = make_sdesc(sA + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
+            const uint64_t ad = Loader::A_TMA_SW128 ? make_sdesc_sw128(sA + (uint32_t)k * 32)
+                                                    : make_sdesc(sA + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
             const uint64_t bd = Loader::B_TMA_SW128 ? make_sdesc_sw128(sB + (uint32_t)k * 32)
                                                     : make_sdesc(sB + (uint32_t)(2 * k) * (BN * 16), BN * 16, 128);
             umma_bf16(d_tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
