@@ -286,6 +286,7 @@ def main():
             "config": workload_config(args, world),
             "train_img_per_s": train_imgs / (ms * 1e-3),
             "candidates_ok": int(allreduce([ok], "sum")[0]),
+            "failures": [r.failure_reason[:120] for r in recs if r is not None and not r.ok],
             "gpu_launches": launches, "clocks": clock_info}
 
     if not args.no_e2e:

@@ -87,16 +87,15 @@ struct DenseDxEpiTc {
   int in, B;
   __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
     const int i = c.m0 + row;
-    if (i >= in) return;
+    const int b0 = c.n0 + col;
+    if (i >= in || b0 >= B) return;
+    const int n = B - b0 < 16 ? B - b0 : 16;
+    float mk[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int b = c.n0 + col + u;
-      if (b >= B) break;
-      const size_t off = (size_t)b * in + i;
-      float t = v[u];
-      if (mask && !(ldf(mask, off) > 0.f)) t = 0.f;
-      stf(dx, off, t);
-    }
+    for (int u = 0; u < 16; ++u) mk[u] = (mask && u < n) ? ldf(mask, (size_t)(b0 + u) * in + i) : 1.f;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (u < n) stf(dx, (size_t)(b0 + u) * in + i, mk[u] > 0.f ? v[u] : 0.f);
   }
   __device__ void finish(int, int) const {}
 };
@@ -142,18 +141,29 @@ struct DenseDwSgdEpi {
   float lr, mu;
   __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
     const int i = c.m0 + row;
-    if (i >= in) return;
+    const int o0 = c.n0 + col;
+    if (i >= in || o0 >= out) return;
+    const int n = out - o0 < 16 ? out - o0 : 16;
+    // issue all 32 independent loads before any dependent arithmetic (memory-level parallelism)
+    float wv[16], vv[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int o = c.n0 + col + u;
-      if (o >= out) break;
-      const size_t off = (size_t)o * in + i;
-      if (gw) gw[off] = v[u];
-      float wv = w[off], vv = vel[off];
-      sgd_update(wv, vv, v[u], lr, mu);
-      w[off] = wv;
-      vel[off] = vv;
-      wb[(size_t)o * in_pad + i] = __float2bfloat16_rn(wv);
+      if (u < n) {
+        const size_t off = (size_t)(o0 + u) * in + i;
+        wv[u] = __ldcs(w + off);
+        vv[u] = __ldcs(vel + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      if (u < n) {
+        const size_t off = (size_t)(o0 + u) * in + i;
+        if (gw) gw[off] = v[u];
+        sgd_update(wv[u], vv[u], v[u], lr, mu);
+        __stcs(w + off, wv[u]);
+        __stcs(vel + off, vv[u]);
+        wb[(size_t)(o0 + u) * in_pad + i] = __float2bfloat16_rn(wv[u]);
+      }
     }
   }
   __device__ void finish(int, int) const {}

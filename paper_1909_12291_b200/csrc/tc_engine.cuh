@@ -8,8 +8,9 @@
 // fp32 accumulator rows. Roles per CTA (persistent, grid <= #SMs):
 //
 //   warps 0-7   producers: cp.async gather into an S-stage smem ring
-//   warps 8-11  epilogue : tcgen05.ld TMEM -> registers -> Epilogue::store
-//   warp  12    MMA      : TMEM alloc + one elected thread issuing tcgen05.mma
+//   warps 8-15  epilogue : tcgen05.ld TMEM -> registers -> Epilogue::store
+//                          (warp w reads TMEM lane quarter w%4, column half (w-8)/4)
+//   warp  16    MMA      : TMEM alloc + one elected thread issuing tcgen05.mma
 //
 // Before the role split every thread helps the Loader fill a small shared
 // table (Loader::init), e.g. the im2col offset of every 16-byte K chunk, so the
@@ -28,8 +29,9 @@ constexpr int TC_BM = 128;  // UMMA M (rows per tile = TMEM lanes)
 constexpr int TC_BK = 64;   // K elements per pipeline stage (8 x 16-byte chunks)
 constexpr int TC_PRODUCERS = 256;
 constexpr int TC_EPI_WARP0 = TC_PRODUCERS / 32;   // first epilogue warp (8)
-constexpr int TC_MMA_WARP = TC_EPI_WARP0 + 4;      // 12
-constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;  // 416
+constexpr int TC_EPI_WARPS = 8;                    // 2 per TMEM lane quarter, each half the columns
+constexpr int TC_MMA_WARP = TC_EPI_WARP0 + TC_EPI_WARPS;  // 16
+constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;        // 544
 constexpr int TC_TABLE_BYTES = 20480;              // loader lookup tables
 constexpr int TC_MAX_LAG = 8;
 
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], TC_EPI_WARPS * 32);
     }
     fence_barrier_init();
   }
@@ -187,6 +189,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp < TC_MMA_WARP) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter (warp % 4 == q)
+    const int half = (warp - TC_EPI_WARP0) >> 2;
+    constexpr int HALF_COLS = BN >= 32 ? BN / 2 : BN;
+    const int col_begin = half * HALF_COLS;
+    const int col_end = BN >= 32 ? col_begin + HALF_COLS : (half == 0 ? BN : 0);
     const int row_in_tile = q * 32 + lane;
     int lt = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++lt) {
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-      for (int col = 0; col < BN; col += 16) {
+      for (int col = col_begin; col < col_end; col += 16) {
         uint32_t r[16];
         tmem_ld16(tbase + col, r);
         tmem_ld_wait();
