@@ -48,6 +48,25 @@ inline bool make_tmap_kmajor(CUtensorMap* map, const bf16* base, int rows, int K
   return r == CUDA_SUCCESS;
 }
 
+// TMA descriptor for an MN-major operand stored [K rows][MN] (MN contiguous):
+// boxes of 64 MN-elements x 64 K-rows with SWIZZLE_128B.
+inline bool make_tmap_mn64(CUtensorMap* map, const bf16* base, int krows, int mn) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)mn, (cuuint64_t)krows};
+  cuuint64_t strides[1] = {(cuuint64_t)mn * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)base, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 inline bool tma_disabled() {
   const char* e = getenv("CE_DISABLE_TMA");
   return e && e[0] == '1';
@@ -148,11 +167,13 @@ struct DgradClass {
   int hc, wc;   // positions of the class per axis
 };
 
+template <bool TMA_B>
 struct DgradTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B;
+  CUtensorMap wmap;  // class block [c][K] when TMA_B
   const bf16* dy;
-  const bf16* wt;  // [c][k*k][co]
+  const bf16* wt;  // this class's block [c][K] of the class-blocked transpose
   ConvGeom g;
   DgradClass cl;
   int K, M, BN;    // K = ti*tj*co, M = n*hc*wc
@@ -168,12 +189,18 @@ struct DgradTcLoader {
       const int i = cl.rh + g.s * a, j = cl.rw + g.s * b;
       doff[k8] = o0 - (a * g.ow + b) * g.co;
       dab[k8] = (a << 16) | b;
-      woff[k8] = (i * g.k + j) * g.co + o0;
+      woff[k8] = kk;
+      (void)i;
+      (void)j;
     }
   }
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
-                       uint64_t*) const {
+                       uint64_t* full) const {
     const int nk8 = K / 8;
+    if (TMA_B && ptid == 0) {
+      mbar_expect_tx(full, (uint32_t)BN * 128u);
+      tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+    }
     const int* doff = (const int*)table;
     const int* dab = doff + nk8;
     const int* woff = dab + nk8;
@@ -201,12 +228,14 @@ struct DgradTcLoader {
         cp_async16(sA + kmajor_off(TC_BM, r, kc), src, ok ? 16u : 0u);
       }
     }
-    for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
-      const int r = ch % BN, kc = ch / BN;
-      const int cc = c.n0 + r, k8 = kb * 8 + kc;
-      const bool ok = cc < g.c && k8 < nk8;
-      cp_async16(sB + kmajor_off(BN, r, kc),
-                 ok ? (const void*)(wt + (size_t)cc * g.k * g.k * g.co + woff[k8]) : (const void*)wt, ok ? 16u : 0u);
+    if (!TMA_B) {
+      for (int ch = ptid; ch < BN * 8; ch += TC_PRODUCERS) {
+        const int r = ch % BN, kc = ch / BN;
+        const int cc = c.n0 + r, k8 = kb * 8 + kc;
+        const bool ok = cc < g.c && k8 < nk8;
+        cp_async16(sB + kmajor_off(BN, r, kc), ok ? (const void*)(wt + (size_t)cc * K + woff[k8]) : (const void*)wt,
+                   ok ? 16u : 0u);
+      }
     }
   }
 };
@@ -245,9 +274,11 @@ struct DgradTcEpi {
 };
 
 // ------------------------------------------------------------------ wgrad
+template <bool TMA_B>
 struct WgradTcLoader {
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B;
+  CUtensorMap dmap;  // dY [Mo][co] as 64x64 MN-major SW128 boxes when TMA_B
   const bf16* x;
   const bf16* dy;
   ConvGeom g;
@@ -257,7 +288,7 @@ struct WgradTcLoader {
   FastDiv d_ow, d_oh;
   __device__ void init(uint8_t*, int, int) const {}
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
-                       uint64_t*) const {
+                       uint64_t* full) const {
     // A: 16 groups of 8 (i,j,c) rows x 64 reduction indices; 256 producers -> 4 chunks each
     {
       const int grp = ptid & 15;
@@ -285,6 +316,13 @@ struct WgradTcLoader {
       }
     }
     // B: BN/8 groups of 8 output channels x 64 reduction indices
+    if (TMA_B) {
+      if (ptid == 0) {
+        mbar_expect_tx(full, (uint32_t)BN * TC_BK * 2u);
+        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &dmap, c.n0 + 64 * j, kb * TC_BK, full);
+      }
+      return;
+    }
     const int groups = BN / 8;
     for (int ch = ptid; ch < groups * TC_BK; ch += TC_PRODUCERS) {
       const int grp = ch % groups, kr = ch / groups;
@@ -371,9 +409,20 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
       int s = with_bn(g.c, [&](auto bn) {
         constexpr int BN = decltype(bn)::value;
         TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
-        DgradTcLoader ld{dy, wt, g, cl, K, M, BN, FastDiv(cl.wc), FastDiv(cl.hc)};
+        const bf16* wcls = wt + dg_class_base(g.k, g.s, g.c, g.co, rh * g.s + rw);
         DgradTcEpi ep{dx, mask, g, cl, M, FastDiv(cl.wc), FastDiv(cl.hc)};
-        cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+        cudaError_t e;
+        DgradTcLoader<true> ldt{};
+        if (!tma_disabled() && make_tmap_kmajor(&ldt.wmap, wcls, g.c, K, BN)) {
+          ldt.dy = dy; ldt.wt = wcls; ldt.g = g; ldt.cl = cl; ldt.K = K; ldt.M = M; ldt.BN = BN;
+          ldt.d_wc = FastDiv(cl.wc); ldt.d_hc = FastDiv(cl.hc);
+          e = tc_launch<BN>(ldt, ep, sh, num_sms, st);
+        } else {
+          DgradTcLoader<false> ld{};
+          ld.dy = dy; ld.wt = wcls; ld.g = g; ld.cl = cl; ld.K = K; ld.M = M; ld.BN = BN;
+          ld.d_wc = FastDiv(cl.wc); ld.d_hc = FastDiv(cl.hc);
+          e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+        }
         return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_dgrad_tc: %s", cudaGetErrorString(e));
       });
       if (s != CE_OK) return s;
@@ -402,9 +451,19 @@ inline int conv_wgrad_tc(const ConvGeom& g, const bf16* x, const bf16* dy, float
     constexpr int BN = decltype(bn)::value;
     TcShape sh = tc_make_shape(Kf, g.co, Mo, BN, want);
     *splits_out = sh.splits;
-    WgradTcLoader ld{x, dy, g, Kf, Mo, BN, FastDiv(g.ow), FastDiv(g.oh)};
     WgradTcEpi ep{part, Kf, g.co};
-    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    cudaError_t e;
+    WgradTcLoader<true> ldt{};
+    if (BN >= 64 && !tma_disabled() && make_tmap_mn64(&ldt.dmap, dy, Mo, g.co)) {
+      ldt.x = x; ldt.dy = dy; ldt.g = g; ldt.Kf = Kf; ldt.Mo = Mo; ldt.BN = BN;
+      ldt.d_ow = FastDiv(g.ow); ldt.d_oh = FastDiv(g.oh);
+      e = tc_launch<BN>(ldt, ep, sh, num_sms, st);
+    } else {
+      WgradTcLoader<false> ld{};
+      ld.x = x; ld.dy = dy; ld.g = g; ld.Kf = Kf; ld.Mo = Mo; ld.BN = BN;
+      ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    }
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_wgrad_tc: %s", cudaGetErrorString(e));
   });
 }

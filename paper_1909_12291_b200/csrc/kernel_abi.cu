@@ -89,7 +89,7 @@ int ce_conv_dgrad(const ce_conv_desc* d, const void* dy, const void* w, const vo
     bf16* wt = (bf16*)workspace;
     // [o][tap][c] bf16 -> [c][tap][o]
     const bf16* wb = (const bf16*)w;
-    transpose_w_bf16_kernel<<<grid_for(wn), 256, 0, st>>>(wb, g.co, g.k * g.k, g.c, wt);
+    transpose_w_bf16_kernel<<<grid_for(wn), 256, 0, st>>>(wb, g.co, g.k, g.s, g.c, wt);
     CE_CHECK_LAUNCH();
     return conv_dgrad_tc(g, (const bf16*)dy, wt, (const bf16*)mask, (bf16*)dx, sms(), st);
   }
@@ -120,7 +120,7 @@ int ce_conv_wgrad(const ce_conv_desc* d, const void* x, const void* dy, float* d
   CE_CHECK_LAUNCH();
   float* bpart = part + (size_t)splits * g.co * K;
   const int bsplits = tc ? colsum((const bf16*)dy, Mo, g.co, bpart, st) : colsum((const float*)dy, Mo, g.co, bpart, st);
-  conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(part, splits, g.co, K, g.c, g.k * g.k, nullptr, nullptr,
+  conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(part, splits, g.co, K, g.c, g.k, g.s, nullptr, nullptr,
                                                                dw, nullptr, nullptr, 0.f, 0.f);
   bias_sgd_kernel<<<cdiv(g.co, 256), 256, 0, st>>>(bpart, bsplits, g.co, nullptr, nullptr, db, 0.f, 0.f);
   CE_CHECK_LAUNCH();

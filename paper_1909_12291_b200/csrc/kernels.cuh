@@ -251,6 +251,22 @@ struct DenseXN {
   __device__ float operator()(int b, int i) const { return ldf(x, (size_t)b * in + i); }
 };
 
+// Class-blocked transposed conv weights (dgrad B operand): for stride s the
+// taps split into s*s residue classes (rh, rw) = (i mod s, j mod s); class cls
+// owns a contiguous [c][ti*tj*co] block (K index (a*tj + b)*co + o with
+// i = rh + s*a, j = rw + s*b), so every class is a plain K-major matrix.
+__host__ __device__ inline int dg_taps(int k, int s, int r) { return r < k ? (k - r + s - 1) / s : 0; }
+__host__ __device__ inline size_t dg_class_base(int k, int s, int c, int co, int cls) {
+  size_t base = 0;
+  for (int q = 0; q < cls; ++q) base += (size_t)c * dg_taps(k, s, q / s) * dg_taps(k, s, q % s) * co;
+  return base;
+}
+__host__ __device__ inline size_t dg_wt_index(int k, int s, int c, int co, int i, int j, int ch, int o) {
+  const int rh = i % s, rw = j % s, a = i / s, b = j / s;
+  const int tj = dg_taps(k, s, rw), kcls = dg_taps(k, s, rh) * tj * co;
+  return dg_class_base(k, s, c, co, rh * s + rw) + (size_t)ch * kcls + ((size_t)a * tj + b) * co + o;
+}
+
 // classical momentum, in fp32 without FMA contraction (nn.py:306-322):
 //   v <- mu*v - lr*g ; w <- w + v
 __device__ __forceinline__ void sgd_update(float& w, float& v, float g, float lr, float mu) {

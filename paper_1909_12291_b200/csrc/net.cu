@@ -374,7 +374,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       float* bpart = net->ws + (size_t)splits * g.co * K;
       Prof pf(net, P_CONV_SGD, 0.0, ab * Mo * g.co + 4.0 * splits * g.co * K + 20.0 * g.co * K, 3);
       int bsplits = colsum(dy, Mo, g.co, bpart, st);
-      conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(net->ws, splits, g.co, K, g.c, g.k * g.k, l.W, l.VW,
+      conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(net->ws, splits, g.co, K, g.c, g.k, g.s, l.W, l.VW,
                                                                    keep ? l.GW : nullptr, l.Wbf, l.Wtbf, lr, mu);
       bias_sgd_kernel<<<cdiv(g.co, 256), 256, 0, st>>>(bpart, bsplits, g.co, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
       CE_CHECK_LAUNCH();
@@ -782,7 +782,7 @@ int ce_net_set_params(ce_net* net, int p, const float* w, const float* b) {
   if (l.Wbp)
     f32_to_bf16_pad_kernel<<<grid_for((size_t)l.out_units * l.in_pad), 256, 0, st>>>(l.W, l.out_units, l.in_units,
                                                                                       l.in_pad, l.Wbp);
-  if (l.Wtbf) conv_wt_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.g.co, l.g.k * l.g.k, l.g.c, l.Wtbf);
+  if (l.Wtbf) conv_wt_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.s, l.g.c, l.Wtbf);
   CE_CHECK_LAUNCH();
   CE_CUDA(cudaStreamSynchronize(st));
   return CE_OK;

@@ -241,7 +241,7 @@ inline int colsum(const T* dy, int M, int N, float* part, cudaStream_t st) {
 
 // conv weights: g = sum_split part[split][o][kk]; momentum update of W (fp32 master)
 // plus bf16 mirrors W[o][kk] and Wt[c][tap][o] (dgrad operand of the tensor path)
-__global__ void conv_sgd_kernel(const float* __restrict__ part, int splits, int co, int K, int cp, int taps,
+__global__ void conv_sgd_kernel(const float* __restrict__ part, int splits, int co, int K, int cp, int k, int s,
                                 float* __restrict__ w, float* __restrict__ vel, float* __restrict__ gw,
                                 bf16* __restrict__ wbf, bf16* __restrict__ wtbf, float lr, float mu) {
   size_t total = (size_t)co * K;
@@ -258,7 +258,7 @@ __global__ void conv_sgd_kernel(const float* __restrict__ part, int splits, int 
     if (wtbf) {
       int o = e / K, kk = e % K;
       int c = kk % cp, tap = kk / cp;
-      wtbf[((size_t)c * taps + tap) * co + o] = __float2bfloat16_rn(wv);
+      wtbf[dg_wt_index(k, s, cp, co, tap / k, tap % k, c, o)] = __float2bfloat16_rn(wv);
     }
   }
 }
@@ -412,26 +412,29 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ a, size_t n, bf16* 
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     b[e] = __float2bfloat16_rn(a[e]);
 }
-__global__ void conv_wt_kernel(const float* __restrict__ w, int co, int taps, int cp, bf16* __restrict__ wt) {
+__global__ void conv_wt_kernel(const float* __restrict__ w, int co, int k, int s, int cp, bf16* __restrict__ wt) {
+  const int taps = k * k;
   size_t total = (size_t)co * taps * cp;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     int c = e % cp;
     size_t t = e / cp;
     int tap = t % taps;
     int o = t / taps;
-    wt[((size_t)c * taps + tap) * co + o] = __float2bfloat16_rn(w[e]);
+    wt[dg_wt_index(k, s, cp, co, tap / k, tap % k, c, o)] = __float2bfloat16_rn(w[e]);
   }
 }
 
-// bf16 [o][tap][c] -> [c][tap][o] (dgrad B operand)
-__global__ void transpose_w_bf16_kernel(const bf16* __restrict__ w, int co, int taps, int cp, bf16* __restrict__ wt) {
+// bf16 [o][tap][c] -> class-blocked transpose (dgrad B operand)
+__global__ void transpose_w_bf16_kernel(const bf16* __restrict__ w, int co, int k, int s, int cp,
+                                        bf16* __restrict__ wt) {
+  const int taps = k * k;
   size_t total = (size_t)co * taps * cp;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     int c = e % cp;
     size_t t = e / cp;
     int tap = t % taps;
     int o = t / taps;
-    wt[((size_t)c * taps + tap) * co + o] = w[e];
+    wt[dg_wt_index(k, s, cp, co, tap / k, tap % k, c, o)] = w[e];
   }
 }
 

@@ -147,6 +147,19 @@ CE_DEV uint64_t make_sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
+// MN-major SWIZZLE_128B canonical layout (TMA box of 64 MN-elements x 64 K-rows):
+// K rows 128 B apart, 8-row K groups 1024 B apart (SBO), 64-wide MN blocks LBO
+// apart; one 16-deep MMA K step advances the start address by 2 K groups.
+CE_DEV uint64_t make_sdesc_sw128_mn(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // Instruction descriptor for kind::f16 with bf16 A/B and fp32 D.
 //   [4,6) D fmt (1 = f32)  [7,10) A fmt (1 = bf16)  [10,13) B fmt (1 = bf16)
 //   [15] A major (0 = K, 1 = MN)  [16] B major  [17,23) N >> 3  [24,29) M >> 4

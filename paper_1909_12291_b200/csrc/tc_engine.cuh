@@ -243,8 +243,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // MN-major: a K=16 step covers K groups 2k, 2k+1 (LBO apart).
             const uint64_t ad = Loader::A_TMA_SW128 ? make_sdesc_sw128(sA + (uint32_t)k * 32)
                                                     : make_sdesc(sA + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
-            const uint64_t bd = Loader::B_TMA_SW128 ? make_sdesc_sw128(sB + (uint32_t)k * 32)
-                                                    : make_sdesc(sB + (uint32_t)(2 * k) * (BN * 16), BN * 16, 128);
+            uint64_t bd;
+            if (Loader::B_TMA_SW128)
+              bd = Loader::B_MN_MAJOR ? make_sdesc_sw128_mn(sB + (uint32_t)k * 2048, 64 * 128)
+                                      : make_sdesc_sw128(sB + (uint32_t)k * 32);
+            else
+              bd = make_sdesc(sB + (uint32_t)(2 * k) * (BN * 16), BN * 16, 128);
             umma_bf16(d_tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
