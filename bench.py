@@ -122,26 +122,24 @@ def run_reference(args, rank):
     splits = default_splits()
     genomes = population(1)
     budget = TrainBudget(epochs=2)
-    chunk = 4
-    times, rates = [], []
+    times, extrapolated = [], []
     for i in range(args.warmup + args.steps):
-        sample = [genomes[(i * chunk + j) % len(genomes)] for j in range(chunk)]
         t0 = time.perf_counter()
-        r, _ = cpu_rate(sample, splits, budget)
+        _, secs = cpu_rate(genomes, splits, budget)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
-            rates.append(r)
-    value = statistics.fmean(rates)
+            extrapolated.append(secs)
+    value = len(genomes) / statistics.fmean(extrapolated) * 3600.0
     cores = os.cpu_count()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.fmean(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": workload_config(args, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{chunk} genomes/step of the C2 population: 1 train step + 1 forward at "
-                                       "batch 8 each on the numpy oracle (OpenBLAS, all host threads), "
-                                       "extrapolated to 2 epochs + val + latency"},
+                             "sample": "every step: all 16 genomes of the C2 population, 1 train step + 1 "
+                                       "forward at batch 8 each on the numpy oracle (OpenBLAS, all host threads), "
+                                       "extrapolated to each candidate's 2 epochs + val + latency"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -311,13 +309,13 @@ def main():
         line["kernel_classes"] = line["roofline"].pop("classes")
 
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        sample = mine[:8]
+        sample = mine
         t0 = time.perf_counter()
         rate, _ = cpu_rate(sample, splits, budget)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                "sample": f"first {len(sample)} genomes of the population: 1 train step + 1 "
+                                "sample": f"all {len(sample)} genomes of the population: 1 train step + 1 "
                                           "forward at batch 8 each on the numpy oracle (all host threads), "
-                                          "extrapolated to 2 epochs + val + latency; "
+                                          "extrapolated to each candidate's 2 epochs + val + latency; "
                                           f"{time.perf_counter() - t0:.1f} s of CPU work"}
     if rank == 0:
         print(json.dumps(line), flush=True)

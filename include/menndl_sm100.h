@@ -96,6 +96,8 @@ int ce_net_num_param_layers(const ce_net* net, int* count);
 /* param layer p: weights in reference layout (conv (o,c,kh,kw), dense (o,in)), bias (o) */
 int ce_net_set_params(ce_net* net, int p, const float* w, const float* b);
 int ce_net_get_params(ce_net* net, int p, float* w, float* b, float* vel_w, float* vel_b);
+/* retain raw parameter gradients of the next steps for ce_net_get_grads (off by default) */
+int ce_net_keep_grads(ce_net* net, int on);
 int ce_net_get_grads(ce_net* net, int p, float* gw, float* gb);
 
 /* inference forward of n samples (float32 NCHW host) -> logits (n, classes) */

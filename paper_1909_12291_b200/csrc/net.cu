@@ -645,7 +645,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
     if (l.kind == CE_LAYER_CONV) total_params += (size_t)l.g.co * l.g.k * l.g.k * l.g.c;
     if (l.kind == CE_LAYER_DENSE) total_params += (size_t)l.out_units * l.in_units;
   }
-  net->keep_grads = total_params <= (64u << 20);
+  net->keep_grads = false;  // opt-in (ce_net_keep_grads): storing dW costs 4 B/param/step
   size_t max_g = (size_t)B * net->in_cp * net->in_h * net->in_w * ab, ws = 0, gbf_elems = 0;
   for (size_t i = 0; i < net->L.size(); ++i) {
     Layer& l = net->L[i];
@@ -691,10 +691,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
       ALLOC(l.VW, l.wn * 4);
       ALLOC(l.b, l.bn * 4);
       ALLOC(l.Vb, l.bn * 4);
-      if (net->keep_grads) {
-        ALLOC(l.GW, l.wn * 4);
-        ALLOC(l.Gb, l.bn * 4);
-      }
+
       if (precision == CE_PREC_BF16 && l.kind == CE_LAYER_CONV) {
         ALLOC(l.Wbf, l.wn * 2);
         ALLOC(l.Wtbf, l.wn * 2);
@@ -820,10 +817,24 @@ int ce_net_get_params(ce_net* net, int p, float* w, float* b, float* vw, float* 
   return CE_OK;
 }
 
+int ce_net_keep_grads(ce_net* net, int on) {
+  if (check_net(net)) return CE_EINVAL;
+  DevGuard dg(net->device);
+  if (on)
+    for (int p : net->params) {
+      Layer& l = net->L[p];
+      if (!l.GW) ALLOC(l.GW, l.wn * 4);
+      if (!l.Gb) ALLOC(l.Gb, l.bn * 4);
+    }
+  net->keep_grads = on != 0;
+  CE_CUDA(cudaStreamSynchronize(net->st));
+  return CE_OK;
+}
+
 int ce_net_get_grads(ce_net* net, int p, float* gw, float* gb) {
   Layer* lp;
   if (int s = param_layer(net, p, &lp)) return s;
-  if (!lp->GW) return fail(CE_EINVAL, "gradients are not retained for nets above 64M parameters");
+  if (!lp->GW) return fail(CE_EINVAL, "gradients are not retained; call ce_net_keep_grads first");
   DevGuard dg(net->device);
   if (gw) if (int s = download_w(net, *lp, lp->GW, gw)) return s;
   if (gb) CE_CUDA(cudaMemcpyAsync(gb, lp->Gb, lp->bn * 4, cudaMemcpyDeviceToHost, net->st));

@@ -54,6 +54,7 @@ _SIGNATURES = {
     "ce_net_num_param_layers": ([_P, C.POINTER(C.c_int)], C.c_int),
     "ce_net_set_params": ([_P, C.c_int, _F, _F], C.c_int),
     "ce_net_get_params": ([_P, C.c_int, _F, _F, _F, _F], C.c_int),
+    "ce_net_keep_grads": ([_P, C.c_int], C.c_int),
     "ce_net_get_grads": ([_P, C.c_int, _F, _F], C.c_int),
     "ce_net_forward_host": ([_P, _F, C.c_int, _F], C.c_int),
     "ce_net_get_activation": ([_P, C.c_int, C.c_int, _F], C.c_int),
@@ -222,6 +223,9 @@ class Net:
         vw, vb = np.empty(w_shape, np.float32), np.empty(b_shape, np.float32)
         check(load().ce_net_get_params(self._h, p, fptr(w), fptr(b), fptr(vw), fptr(vb)))
         return w, b, vw, vb
+
+    def keep_grads(self, on=True):
+        check(load().ce_net_keep_grads(self._h, int(bool(on))))
 
     def get_grads(self, p, w_shape, b_shape):
         gw, gb = np.empty(w_shape, np.float32), np.empty(b_shape, np.float32)

@@ -38,6 +38,11 @@ CASES = [
     ("stride3_k7", "id=case0000000005 " + _BASE +
      "f0=conv:oc=24,k=7,s=3,relu=1 f1=conv:oc=128,k=3,s=2,relu=1 f2=conv:oc=256,k=2,s=1,relu=0 "
      "h0=dense:units=40", (3, 48, 48)),
+    ("odd_units", "id=case0000000006 " + _BASE +
+     "f0=conv:oc=64,k=5,s=3,relu=1 h0=dense:units=37", (3, 40, 40)),
+    # C2 population genome #15 (2d5ebb4eae1bf684): 262,144 -> 523 head
+    ("c2_g15", "id=2d5ebb4eae1bf684 parents= lr=0.017072315886796932 momentum=0.5 batch_size=32 "
+     "f0=conv:oc=256,k=5,s=3,relu=1 h0=dense:units=523", (3, 100, 100)),
 ]
 
 

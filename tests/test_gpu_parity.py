@@ -44,6 +44,7 @@ def test_forward_backward_step(name, text, shape, precision):
     x, y = make_batch(N, shape, seed=11)
     tol = TOL[precision]
     dev = net.to_device(0, precision, max_batch=N)
+    dev.keep_grads()
     try:
         # ---- T1 forward: every layer output and the logits
         logits = dev.forward(x)

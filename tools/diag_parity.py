@@ -20,6 +20,7 @@ for name, text, shape in CASES:
     o = OracleNet.from_network(net)
     x, y = make_batch(N, shape, seed=11)
     dev = net.to_device(0, prec, max_batch=N)
+    dev.keep_grads()
     lg = dev.forward(x)
     ro = o.forward(x)
     acts = []
