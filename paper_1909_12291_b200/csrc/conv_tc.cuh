@@ -67,25 +67,60 @@ inline bool make_tmap_mn64(CUtensorMap* map, const bf16* base, int krows, int mn
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// TMA im2col descriptor over an NHWC bf16 activation for a valid (unpadded)
+// convolution with kernel k and stride s: `pixels` output pixels x 64 channels
+// per copy (128 B rows, SWIZZLE_128B), receptive-field origins traversed in
+// (n, p, q) order with stride s (bounding box shrunk by k-1 on the far side).
+inline bool make_tmap_im2col(CUtensorMap* map, const bf16* x, const ConvGeom& g, int pixels) {
+  static PFN_cuTensorMapEncodeIm2col_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)g.c, (cuuint64_t)g.w, (cuuint64_t)g.h, (cuuint64_t)g.n};
+  cuuint64_t strides[3] = {(cuuint64_t)g.c * 2, (cuuint64_t)g.w * g.c * 2, (cuuint64_t)g.h * g.w * g.c * 2};
+  int lower[2] = {0, 0};
+  int upper[2] = {-(g.k - 1), -(g.k - 1)};
+  cuuint32_t estr[4] = {1, (cuuint32_t)g.s, (cuuint32_t)g.s, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)x, dims, strides, lower, upper, 64,
+                      (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  // driver <= 13.1 workaround (as in CUTLASS): small tensors must not set bit 21 of word 1
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && (size_t)g.n * g.h * g.w * g.c * 2 < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  return true;
+}
+
 inline bool tma_disabled() {
   const char* e = getenv("CE_DISABLE_TMA");
+  return e && e[0] == '1';
+}
+inline bool im2col_disabled() {
+  const char* e = getenv("CE_DISABLE_IM2COL");
   return e && e[0] == '1';
 }
 
 // ------------------------------------------------------------------ forward
 // table: xoff[k8] = im2col offset of K chunk k8 = (tap, c0) relative to the
 // output pixel's receptive-field origin: (i*W + j)*C + c0.
-template <bool TMA_B>
+template <int MODE>
 struct FwdTcLoader {
+  static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2;
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B;
+  static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL;
   CUtensorMap wmap;  // B operand (weights) when TMA_B
+  CUtensorMap xmap;  // im2col view of x when IM2COL
   const bf16* x;
   const bf16* w;  // [o][K]
   ConvGeom g;
   int K, M, BN;
   FastDiv d_ow, d_oh;
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
+    if (IM2COL) return;
     int* xoff = (int*)table;
     for (int k8 = tid; k8 < K / 8; k8 += nthreads) {
       const int kk = k8 * 8, tap = kk / g.c, c0 = kk - tap * g.c;
@@ -96,6 +131,18 @@ struct FwdTcLoader {
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
                        uint64_t* full) const {
     const int* xoff = (const int*)table;
+    if (IM2COL) {  // one thread: A via im2col TMA (tap, 64-channel slab), B via 2-D TMA
+      const int cpb = g.c / 64;
+      const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
+      const int i = tap / g.k, j = tap - i * g.k;
+      uint32_t q, p, n, t;
+      d_ow.divmod((uint32_t)c.m0, t, q);
+      d_oh.divmod(t, n, p);
+      mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
+      tma_load_im2col_4d(sA, &xmap, c0, (int)q * g.s, (int)p * g.s, (int)n, (uint16_t)j, (uint16_t)i, full);
+      tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+      return;
+    }
     if (TMA_B) {
       if (ptid == 0) {
         mbar_expect_tx(full, (uint32_t)BN * 128u);
@@ -170,7 +217,7 @@ struct DgradClass {
 template <bool TMA_B>
 struct DgradTcLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B, PURE_TMA = false;
   CUtensorMap wmap;  // class block [c][K] when TMA_B
   const bf16* dy;
   const bf16* wt;  // this class's block [c][K] of the class-blocked transpose
@@ -274,11 +321,13 @@ struct DgradTcEpi {
 };
 
 // ------------------------------------------------------------------ wgrad
-template <bool TMA_B>
+template <int MODE>
 struct WgradTcLoader {
+  static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2;
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B;
+  static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL;
   CUtensorMap dmap;  // dY [Mo][co] as 64x64 MN-major SW128 boxes when TMA_B
+  CUtensorMap xmap;  // im2col view of x (64 pixels x 64 channels) when IM2COL
   const bf16* x;
   const bf16* dy;
   ConvGeom g;
@@ -289,6 +338,26 @@ struct WgradTcLoader {
   __device__ void init(uint8_t*, int, int) const {}
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
                        uint64_t* full) const {
+    if (IM2COL) {  // one thread: two 64-row (tap, channel-slab) blocks of A + BN/64 blocks of dY
+      uint32_t q, p, n, t;
+      d_ow.divmod((uint32_t)(kb * TC_BK), t, q);
+      d_oh.divmod(t, n, p);
+      uint32_t bytes = (uint32_t)BN * TC_BK * 2u;
+      int nblk = 0;
+      for (int blk = 0; blk < 2; ++blk)
+        if (c.m0 + 64 * blk < Kf) ++nblk;
+      bytes += (uint32_t)nblk * 64u * TC_BK * 2u;
+      mbar_expect_tx(full, bytes);
+      for (int blk = 0; blk < nblk; ++blk) {
+        const int kk0 = c.m0 + 64 * blk;
+        const int tap = kk0 / g.c, c0 = kk0 - tap * g.c;
+        const int i = tap / g.k, j = tap - i * g.k;
+        tma_load_im2col_4d(sA + blk * 8192, &xmap, c0, (int)q * g.s, (int)p * g.s, (int)n, (uint16_t)j,
+                           (uint16_t)i, full);
+      }
+      for (int jb = 0; jb < BN / 64; ++jb) tma_load_2d(sB + jb * 8192, &dmap, c.n0 + 64 * jb, kb * TC_BK, full);
+      return;
+    }
     // A: 16 groups of 8 (i,j,c) rows x 64 reduction indices; 256 producers -> 4 chunks each
     {
       const int grp = ptid & 15;
@@ -369,15 +438,23 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
     TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
     FwdTcEpi ep{y, bias, M, g.co, relu};
     cudaError_t e;
-    FwdTcLoader<true> ldt{};
-    if (!tma_disabled() && make_tmap_kmajor(&ldt.wmap, w, g.co, K, BN)) {
-      ldt.x = x; ldt.w = w; ldt.g = g; ldt.K = K; ldt.M = M; ldt.BN = BN;
-      ldt.d_ow = FastDiv(g.ow); ldt.d_oh = FastDiv(g.oh);
-      e = tc_launch<BN>(ldt, ep, sh, num_sms, st);
-    } else {
-      FwdTcLoader<false> ld{};
+    const bool tma = !tma_disabled();
+    auto fill = [&](auto& ld) {
       ld.x = x; ld.w = w; ld.g = g; ld.K = K; ld.M = M; ld.BN = BN;
       ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+    };
+    FwdTcLoader<2> ld2{};
+    FwdTcLoader<1> ld1{};
+    if (tma && g.c % 64 == 0 && !im2col_disabled() && make_tmap_kmajor(&ld2.wmap, w, g.co, K, BN) &&
+        make_tmap_im2col(&ld2.xmap, x, g, TC_BM)) {
+      fill(ld2);
+      e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
+    } else if (tma && make_tmap_kmajor(&ld1.wmap, w, g.co, K, BN)) {
+      fill(ld1);
+      e = tc_launch<BN>(ld1, ep, sh, num_sms, st);
+    } else {
+      FwdTcLoader<0> ld{};
+      fill(ld);
       e = tc_launch<BN>(ld, ep, sh, num_sms, st);
     }
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc: %s", cudaGetErrorString(e));
@@ -453,15 +530,23 @@ inline int conv_wgrad_tc(const ConvGeom& g, const bf16* x, const bf16* dy, float
     *splits_out = sh.splits;
     WgradTcEpi ep{part, Kf, g.co};
     cudaError_t e;
-    WgradTcLoader<true> ldt{};
-    if (BN >= 64 && !tma_disabled() && make_tmap_mn64(&ldt.dmap, dy, Mo, g.co)) {
-      ldt.x = x; ldt.dy = dy; ldt.g = g; ldt.Kf = Kf; ldt.Mo = Mo; ldt.BN = BN;
-      ldt.d_ow = FastDiv(g.ow); ldt.d_oh = FastDiv(g.oh);
-      e = tc_launch<BN>(ldt, ep, sh, num_sms, st);
-    } else {
-      WgradTcLoader<false> ld{};
+    const bool tma = !tma_disabled() && BN >= 64;
+    auto fill = [&](auto& ld) {
       ld.x = x; ld.dy = dy; ld.g = g; ld.Kf = Kf; ld.Mo = Mo; ld.BN = BN;
       ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+    };
+    WgradTcLoader<2> ld2{};
+    WgradTcLoader<1> ld1{};
+    if (tma && g.c % 64 == 0 && !im2col_disabled() && make_tmap_mn64(&ld2.dmap, dy, Mo, g.co) &&
+        make_tmap_im2col(&ld2.xmap, x, g, TC_BK)) {
+      fill(ld2);
+      e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
+    } else if (tma && make_tmap_mn64(&ld1.dmap, dy, Mo, g.co)) {
+      fill(ld1);
+      e = tc_launch<BN>(ld1, ep, sh, num_sms, st);
+    } else {
+      WgradTcLoader<0> ld{};
+      fill(ld);
       e = tc_launch<BN>(ld, ep, sh, num_sms, st);
     }
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_wgrad_tc: %s", cudaGetErrorString(e));

@@ -19,17 +19,15 @@ namespace ce {
 
 struct DenseFwdLoader {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true;
+  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true;
   CUtensorMap amap, bmap;
   int BN;
   __device__ void init(uint8_t*, int, int) const {}
-  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
                        uint64_t* full) const {
-    if (ptid == 0) {
-      mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
-      tma_load_2d(sA, &amap, kb * TC_BK, c.m0, full);
-      tma_load_2d(sB, &bmap, kb * TC_BK, c.n0, full);
-    }
+    mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
+    tma_load_2d(sA, &amap, kb * TC_BK, c.m0, full);
+    tma_load_2d(sB, &bmap, kb * TC_BK, c.n0, full);
   }
 };
 
@@ -51,7 +49,7 @@ struct DenseFwdEpi {
 
 struct DenseDxLoader {
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false, PURE_TMA = false;
   const bf16* wb;  // [out][in_pad]
   const bf16* gb;  // [B][out_pad]
   int in, in_pad, out, out_pad, B, BN;
@@ -102,7 +100,7 @@ struct DenseDxEpiTc {
 
 struct DenseDwLoader {
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false, PURE_TMA = false;
   const bf16* x;   // [B][x_stride]
   const bf16* gb;  // [B][out_pad]
   int in, x_stride, out_pad, B, BN;

@@ -56,6 +56,16 @@ CE_DEV void tma_load_2d(uint32_t dst, const void* tmap, int x, int y, uint64_t* 
       "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// im2col-mode 4-D copy (NHWC): `pixels_per_column` output pixels starting at the
+// receptive-field origin (c, w, h, n), shifted by the filter tap (off_w, off_h).
+CE_DEV void tma_load_im2col_4d(uint32_t dst, const void* tmap, int c, int w, int h, int n, uint16_t off_w,
+                               uint16_t off_h, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(tmap), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar)), "h"(off_w), "h"(off_h)
+      : "memory");
+}
 CE_DEV void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], TC_PRODUCERS);
+      mbar_init(&full[i], Loader::PURE_TMA ? 1 : TC_PRODUCERS);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp < TC_EPI_WARP0) {
     // ------------------------------------------------------------ producers
+    if (Loader::PURE_TMA && threadIdx.x != 0) goto teardown;  // one thread issues every copy
     constexpr int LAG = L::LAG;
     const int ptid = threadIdx.x;
     int stage = 0;
@@ -165,18 +166,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
         const uint32_t sB = sA + L::A_BYTES;
-        ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
-        cp_async_commit();
-        // retire the oldest group once LAG newer ones are in flight
-        if (npending == LAG) {
-          cp_async_wait<LAG>();
-          fence_proxy_async();
-          mbar_arrive(&full[pending_stage[0]]);
+        if (Loader::PURE_TMA) {  // copies complete on the barrier themselves
+          ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
+          mbar_arrive(&full[stage]);
+        } else {
+          ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
+          cp_async_commit();
+          // retire the oldest group once LAG newer ones are in flight
+          if (npending == LAG) {
+            cp_async_wait<LAG>();
+            fence_proxy_async();
+            mbar_arrive(&full[pending_stage[0]]);
 #pragma unroll
-          for (int i = 0; i < LAG - 1; ++i) pending_stage[i] = pending_stage[i + 1];
-          --npending;
+            for (int i = 0; i < LAG - 1; ++i) pending_stage[i] = pending_stage[i + 1];
+            --npending;
+          }
+          pending_stage[npending++] = stage;
         }
-        pending_stage[npending++] = stage;
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -241,8 +247,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int k = 0; k < nk16; ++k) {
             // K-major: a K=16 step covers chunks 2k, 2k+1 (LBO apart).
             // MN-major: a K=16 step covers K groups 2k, 2k+1 (LBO apart).
-            const uint64_t ad = Loader::A_TMA_SW128 ? make_sdesc_sw128(sA + (uint32_t)k * 32)
-                                                    : make_sdesc(sA + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
+            uint64_t ad;
+            if (Loader::A_TMA_SW128)
+              ad = Loader::A_MN_MAJOR ? make_sdesc_sw128_mn(sA + (uint32_t)k * 2048, 64 * 128)
+                                      : make_sdesc_sw128(sA + (uint32_t)k * 32);
+            else
+              ad = make_sdesc(sA + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
             uint64_t bd;
             if (Loader::B_TMA_SW128)
               bd = Loader::B_MN_MAJOR ? make_sdesc_sw128_mn(sB + (uint32_t)k * 2048, 64 * 128)
@@ -262,6 +272,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   }
+teardown:
   tc_fence_before();
   __syncthreads();
   if (warp == TC_MMA_WARP) {

@@ -15,7 +15,7 @@ template <int AMN, int BMN>
 struct PlainLoader {
   static constexpr int A_MN_MAJOR = AMN;
   static constexpr int B_MN_MAJOR = BMN;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false, PURE_TMA = false;
   const __nv_bfloat16* A;
   const __nv_bfloat16* B;
   int M, N, K;
