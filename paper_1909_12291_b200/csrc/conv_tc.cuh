@@ -214,11 +214,13 @@ struct DgradClass {
   int hc, wc;   // positions of the class per axis
 };
 
-template <bool TMA_B>
+template <int MODE>
 struct DgradTcLoader {
+  static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2;
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B, PURE_TMA = false;
+  static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL;
   CUtensorMap wmap;  // class block [c][K] when TMA_B
+  CUtensorMap dmap;  // im2col view of dY for this class when IM2COL
   const bf16* dy;
   const bf16* wt;  // this class's block [c][K] of the class-blocked transpose
   ConvGeom g;
@@ -226,13 +228,14 @@ struct DgradTcLoader {
   int K, M, BN;    // K = ti*tj*co, M = n*hc*wc
   FastDiv d_wc, d_hc;
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
+    if (IM2COL) return;
     const int nk8 = K / 8;
     int* doff = (int*)table;
     int* dab = doff + nk8;
     int* woff = dab + nk8;
     for (int k8 = tid; k8 < nk8; k8 += nthreads) {
       const int kk = k8 * 8, tap = kk / g.co, o0 = kk - tap * g.co;
-      const int a = tap / cl.tj, b = tap - a * cl.tj;
+      const int a = cl.ti - 1 - tap / cl.tj, b = cl.tj - 1 - (tap - (tap / cl.tj) * cl.tj);  // flipped taps
       const int i = cl.rh + g.s * a, j = cl.rw + g.s * b;
       doff[k8] = o0 - (a * g.ow + b) * g.co;
       dab[k8] = (a << 16) | b;
@@ -244,6 +247,19 @@ struct DgradTcLoader {
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
                        uint64_t* full) const {
     const int nk8 = K / 8;
+    if (IM2COL) {  // one thread: A = im2col of dY (flipped class taps, 64 channels), B = class weights
+      const int cpb = g.co / 64;
+      const int tap = kb / cpb, o0 = (kb - tap * cpb) * 64;
+      const int ap = tap / cl.tj, bp = tap - ap * cl.tj;
+      uint32_t ww, hh, n, t;
+      d_wc.divmod((uint32_t)c.m0, t, ww);
+      d_hc.divmod(t, n, hh);
+      mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
+      tma_load_im2col_4d(sA, &dmap, o0, (int)ww - (cl.tj - 1), (int)hh - (cl.ti - 1), (int)n, (uint16_t)bp,
+                         (uint16_t)ap, full);
+      tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+      return;
+    }
     if (TMA_B && ptid == 0) {
       mbar_expect_tx(full, (uint32_t)BN * 128u);
       tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
@@ -286,6 +302,35 @@ struct DgradTcLoader {
     }
   }
 };
+
+// im2col view of dY for one dgrad residue class: a stride-1 "full" convolution
+// with a ti x tj kernel, i.e. padding ti-1 / tj-1 on the near side and a far
+// edge that yields exactly hc x wc receptive-field origins.
+inline bool make_tmap_im2col_dgrad(CUtensorMap* map, const bf16* dy, const ConvGeom& g, const DgradClass& cl) {
+  static PFN_cuTensorMapEncodeIm2col_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)g.co, (cuuint64_t)g.ow, (cuuint64_t)g.oh, (cuuint64_t)g.n};
+  cuuint64_t strides[3] = {(cuuint64_t)g.co * 2, (cuuint64_t)g.ow * g.co * 2, (cuuint64_t)g.oh * g.ow * g.co * 2};
+  int lower[2] = {-(cl.tj - 1), -(cl.ti - 1)};
+  int upper[2] = {cl.wc - g.ow - (cl.tj - 1), cl.hc - g.oh - (cl.ti - 1)};
+  if (lower[0] < -128 || lower[1] < -128 || upper[0] < -128 || upper[1] < -128 || upper[0] > 127 || upper[1] > 127)
+    return false;
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)dy, dims, strides, lower, upper, 64, TC_BM, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && (size_t)g.n * g.oh * g.ow * g.co * 2 < 131072)
+    reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  return true;
+}
 
 struct DgradTcEpi {
   bf16* dx;
@@ -489,15 +534,23 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
         const bf16* wcls = wt + dg_class_base(g.k, g.s, g.c, g.co, rh * g.s + rw);
         DgradTcEpi ep{dx, mask, g, cl, M, FastDiv(cl.wc), FastDiv(cl.hc)};
         cudaError_t e;
-        DgradTcLoader<true> ldt{};
-        if (!tma_disabled() && make_tmap_kmajor(&ldt.wmap, wcls, g.c, K, BN)) {
-          ldt.dy = dy; ldt.wt = wcls; ldt.g = g; ldt.cl = cl; ldt.K = K; ldt.M = M; ldt.BN = BN;
-          ldt.d_wc = FastDiv(cl.wc); ldt.d_hc = FastDiv(cl.hc);
-          e = tc_launch<BN>(ldt, ep, sh, num_sms, st);
-        } else {
-          DgradTcLoader<false> ld{};
+        const bool tma = !tma_disabled();
+        auto fill = [&](auto& ld) {
           ld.dy = dy; ld.wt = wcls; ld.g = g; ld.cl = cl; ld.K = K; ld.M = M; ld.BN = BN;
           ld.d_wc = FastDiv(cl.wc); ld.d_hc = FastDiv(cl.hc);
+        };
+        DgradTcLoader<2> ld2{};
+        DgradTcLoader<1> ld1{};
+        if (tma && g.co % 64 == 0 && !im2col_disabled() && make_tmap_kmajor(&ld2.wmap, wcls, g.c, K, BN) &&
+            make_tmap_im2col_dgrad(&ld2.dmap, dy, g, cl)) {
+          fill(ld2);
+          e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
+        } else if (tma && make_tmap_kmajor(&ld1.wmap, wcls, g.c, K, BN)) {
+          fill(ld1);
+          e = tc_launch<BN>(ld1, ep, sh, num_sms, st);
+        } else {
+          DgradTcLoader<0> ld{};
+          fill(ld);
           e = tc_launch<BN>(ld, ep, sh, num_sms, st);
         }
         return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_dgrad_tc: %s", cudaGetErrorString(e));

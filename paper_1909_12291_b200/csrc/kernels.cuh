@@ -253,8 +253,9 @@ struct DenseXN {
 
 // Class-blocked transposed conv weights (dgrad B operand): for stride s the
 // taps split into s*s residue classes (rh, rw) = (i mod s, j mod s); class cls
-// owns a contiguous [c][ti*tj*co] block (K index (a*tj + b)*co + o with
-// i = rh + s*a, j = rw + s*b), so every class is a plain K-major matrix.
+// owns a contiguous [c][ti*tj*co] block, K index (a'*tj + b')*co + o with the
+// class's taps flipped (a' = ti-1-a, b' = tj-1-b; i = rh + s*a, j = rw + s*b):
+// each class is then a plain stride-1 "full" convolution of dY.
 __host__ __device__ inline int dg_taps(int k, int s, int r) { return r < k ? (k - r + s - 1) / s : 0; }
 __host__ __device__ inline size_t dg_class_base(int k, int s, int c, int co, int cls) {
   size_t base = 0;
@@ -263,8 +264,8 @@ __host__ __device__ inline size_t dg_class_base(int k, int s, int c, int co, int
 }
 __host__ __device__ inline size_t dg_wt_index(int k, int s, int c, int co, int i, int j, int ch, int o) {
   const int rh = i % s, rw = j % s, a = i / s, b = j / s;
-  const int tj = dg_taps(k, s, rw), kcls = dg_taps(k, s, rh) * tj * co;
-  return dg_class_base(k, s, c, co, rh * s + rw) + (size_t)ch * kcls + ((size_t)a * tj + b) * co + o;
+  const int ti = dg_taps(k, s, rh), tj = dg_taps(k, s, rw), kcls = ti * tj * co;
+  return dg_class_base(k, s, c, co, rh * s + rw) + (size_t)ch * kcls + ((size_t)(ti - 1 - a) * tj + (tj - 1 - b)) * co + o;
 }
 
 // classical momentum, in fp32 without FMA contraction (nn.py:306-322):
