@@ -47,15 +47,25 @@ struct DenseFwdEpi {
   __device__ void finish(int, int) const {}
 };
 
+template <bool TMA>
 struct DenseDxLoader {
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false, PURE_TMA = false;
+  static constexpr bool A_TMA_SW128 = TMA, B_TMA_SW128 = TMA, PURE_TMA = TMA;
+  CUtensorMap amap;  // Wb [out rows (K)][in_pad (MN)], 64x64 MN-major boxes
+  CUtensorMap bmap;  // gb [B rows][out_pad (K)], K-major boxes
   const bf16* wb;  // [out][in_pad]
   const bf16* gb;  // [B][out_pad]
   int in, in_pad, out, out_pad, B, BN;
   __device__ void init(uint8_t*, int, int) const {}
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
-                       uint64_t*) const {
+                       uint64_t* full) const {
+    if (TMA) {
+      mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
+      tma_load_2d(sA, &amap, c.m0, kb * TC_BK, full);
+      tma_load_2d(sA + 8192, &amap, c.m0 + 64, kb * TC_BK, full);
+      tma_load_2d(sB, &bmap, kb * TC_BK, c.n0, full);
+      return;
+    }
     {  // A: 16 groups of 8 input features x 64 output units
       const int grp = ptid & 15;
       const int i0 = c.m0 + grp * 8;
@@ -138,11 +148,14 @@ struct DenseDwSgdEpi {
   int in, in_pad, out;
   float lr, mu;
   __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
-    const int i = c.m0 + row;
     const int o0 = c.n0 + col;
+    if ((in & 3) == 0) {
+      store_vec(c, row, o0, v);
+      return;
+    }
+    const int i = c.m0 + row;
     if (i >= in || o0 >= out) return;
     const int n = out - o0 < 16 ? out - o0 : 16;
-    // issue all 32 independent loads before any dependent arithmetic (memory-level parallelism)
     float wv[16], vv[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -162,6 +175,56 @@ struct DenseDwSgdEpi {
         __stcs(vel + off, vv[u]);
         wb[(size_t)(o0 + u) * in_pad + i] = __float2bfloat16_rn(wv[u]);
       }
+    }
+  }
+
+  // Lanes 4g..4g+3 hold rows i0..i0+3 (one each) x 16 columns. A rotated
+  // in-quad shuffle transpose gives lane 4g+r rows i0..i0+3 x columns 4r..4r+3,
+  // so W / V move as float4 along `in` (4x fewer, 4x wider memory operations).
+  __device__ void store_vec(const TileCoord& c, int row, int o0, const float (&v)[16]) const {
+    const int lane = threadIdx.x & 31, u = lane & 3, quad = lane & ~3;
+    float g4[4][4];  // g4[row offset][col offset]
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) g4[a][b] = 0.f;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int give = (u - s) & 3;  // destination's column block
+      const int from = (u + s) & 3;  // source row offset
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float send = give == 0 ? v[q] : give == 1 ? v[4 + q] : give == 2 ? v[8 + q] : v[12 + q];
+        const float got = __shfl_sync(0xffffffffu, send, quad | from);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) g4[a][q] = from == a ? got : g4[a][q];
+      }
+    }
+    const int i0 = c.m0 + (row & ~3);
+    const int ob = o0 + 4 * u;
+    if (i0 >= in) return;
+    float4 wv[4], vv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (ob + q < out) {
+        const size_t off = (size_t)(ob + q) * in + i0;
+        wv[q] = __ldcs((const float4*)(w + off));
+        vv[q] = __ldcs((const float4*)(vel + off));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (ob + q >= out) continue;
+      const size_t off = (size_t)(ob + q) * in + i0;
+      float* pw = &wv[q].x;
+      float* pv = &vv[q].x;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) sgd_update(pw[a], pv[a], g4[a][q], lr, mu);
+      if (gw) *(float4*)(gw + off) = make_float4(g4[0][q], g4[1][q], g4[2][q], g4[3][q]);
+      __stcs((float4*)(w + off), wv[q]);
+      __stcs((float4*)(vel + off), vv[q]);
+      __align__(8) __nv_bfloat162 h[2] = {__floats2bfloat162_rn(pw[0], pw[1]), __floats2bfloat162_rn(pw[2], pw[3])};
+      *(uint2*)(wb + (size_t)(ob + q) * in_pad + i0) = *(const uint2*)h;
     }
   }
   __device__ void finish(int, int) const {}
@@ -200,9 +263,20 @@ inline int dense_dx_tc(const bf16* wb, const bf16* gb, int in, int in_pad, int o
   return with_bn(B, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     TcShape sh = tc_make_shape(in, B, out_pad, BN, 1);
-    DenseDxLoader ld{wb, gb, in, in_pad, out, out_pad, B, BN};
     DenseDxEpiTc<TO, TM> ep{dx, mask, in, B};
-    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    cudaError_t e;
+    DenseDxLoader<true> ldt{};
+    if (!tma_disabled() && make_tmap_mn64(&ldt.amap, wb, out, in_pad) &&
+        make_tmap_kmajor(&ldt.bmap, gb, B, out_pad, BN, out_pad)) {
+      ldt.wb = wb; ldt.gb = gb; ldt.in = in; ldt.in_pad = in_pad; ldt.out = out; ldt.out_pad = out_pad;
+      ldt.B = B; ldt.BN = BN;
+      e = tc_launch<BN>(ldt, ep, sh, num_sms, st);
+    } else {
+      DenseDxLoader<false> ld{};
+      ld.wb = wb; ld.gb = gb; ld.in = in; ld.in_pad = in_pad; ld.out = out; ld.out_pad = out_pad;
+      ld.B = B; ld.BN = BN;
+      e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    }
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "dense_dx_tc: %s", cudaGetErrorString(e));
   });
 }
