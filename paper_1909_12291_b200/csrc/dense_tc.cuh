@@ -149,10 +149,6 @@ struct DenseDwSgdEpi {
   float lr, mu;
   __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
     const int o0 = c.n0 + col;
-    if ((in & 3) == 0) {
-      store_vec(c, row, o0, v);
-      return;
-    }
     const int i = c.m0 + row;
     if (i >= in || o0 >= out) return;
     const int n = out - o0 < 16 ? out - o0 : 16;
@@ -178,55 +174,6 @@ struct DenseDwSgdEpi {
     }
   }
 
-  // Lanes 4g..4g+3 hold rows i0..i0+3 (one each) x 16 columns. A rotated
-  // in-quad shuffle transpose gives lane 4g+r rows i0..i0+3 x columns 4r..4r+3,
-  // so W / V move as float4 along `in` (4x fewer, 4x wider memory operations).
-  __device__ void store_vec(const TileCoord& c, int row, int o0, const float (&v)[16]) const {
-    const int lane = threadIdx.x & 31, u = lane & 3, quad = lane & ~3;
-    float g4[4][4];  // g4[row offset][col offset]
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) g4[a][b] = 0.f;
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int give = (u - s) & 3;  // destination's column block
-      const int from = (u + s) & 3;  // source row offset
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float send = give == 0 ? v[q] : give == 1 ? v[4 + q] : give == 2 ? v[8 + q] : v[12 + q];
-        const float got = __shfl_sync(0xffffffffu, send, quad | from);
-#pragma unroll
-        for (int a = 0; a < 4; ++a) g4[a][q] = from == a ? got : g4[a][q];
-      }
-    }
-    const int i0 = c.m0 + (row & ~3);
-    const int ob = o0 + 4 * u;
-    if (i0 >= in) return;
-    float4 wv[4], vv[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (ob + q < out) {
-        const size_t off = (size_t)(ob + q) * in + i0;
-        wv[q] = __ldcs((const float4*)(w + off));
-        vv[q] = __ldcs((const float4*)(vel + off));
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (ob + q >= out) continue;
-      const size_t off = (size_t)(ob + q) * in + i0;
-      float* pw = &wv[q].x;
-      float* pv = &vv[q].x;
-#pragma unroll
-      for (int a = 0; a < 4; ++a) sgd_update(pw[a], pv[a], g4[a][q], lr, mu);
-      if (gw) *(float4*)(gw + off) = make_float4(g4[0][q], g4[1][q], g4[2][q], g4[3][q]);
-      __stcs((float4*)(w + off), wv[q]);
-      __stcs((float4*)(vel + off), vv[q]);
-      __align__(8) __nv_bfloat162 h[2] = {__floats2bfloat162_rn(pw[0], pw[1]), __floats2bfloat162_rn(pw[2], pw[3])};
-      *(uint2*)(wb + (size_t)(ob + q) * in_pad + i0) = *(const uint2*)h;
-    }
-  }
   __device__ void finish(int, int) const {}
 };
 
