@@ -141,6 +141,7 @@ struct DenseDwLoader {
 };
 
 struct DenseDwSgdEpi {
+  static constexpr int EPI_WARPS = 16;  // memory-bound epilogue: more warps = more loads in flight
   float* w;      // [out][in] fp32 master
   float* vel;
   float* gw;     // optional raw gradient

@@ -21,17 +21,38 @@
 // (see ptx.cuh::make_sdesc): a stage holds A as [kchunk][128 rows][16 B] and B
 // as [kchunk][BN rows][16 B] (K-major) or the MN-major analogue.
 #pragma once
+#include <type_traits>
 #include "ptx.cuh"
 
 namespace ce {
 
 constexpr int TC_BM = 128;  // UMMA M (rows per tile = TMEM lanes)
 constexpr int TC_BK = 64;   // K elements per pipeline stage (8 x 16-byte chunks)
-constexpr int TC_PRODUCERS = 256;
-constexpr int TC_EPI_WARP0 = TC_PRODUCERS / 32;   // first epilogue warp (8)
-constexpr int TC_EPI_WARPS = 8;                    // 2 per TMEM lane quarter, each half the columns
-constexpr int TC_MMA_WARP = TC_EPI_WARP0 + TC_EPI_WARPS;  // 16
-constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;        // 544
+constexpr int TC_PRODUCERS = 256;  // producer threads of gather (cp.async) loaders
+
+// Warp roles per (Loader, Epilogue) pair: gather loaders use 8 producer warps,
+// pure-TMA loaders one (a single thread issues every copy); epilogues default
+// to 8 warps (2 per TMEM lane quarter) and may ask for more via Epi::EPI_WARPS.
+template <class Loader>
+struct ProducerWarps {
+  static constexpr int value = Loader::PURE_TMA ? 1 : TC_PRODUCERS / 32;
+};
+template <class Epi, class = void>
+struct EpiWarps {
+  static constexpr int value = 8;
+};
+template <class Epi>
+struct EpiWarps<Epi, std::void_t<decltype(Epi::EPI_WARPS)>> {
+  static constexpr int value = Epi::EPI_WARPS;
+};
+template <class Loader, class Epi>
+struct TcRoles {
+  static constexpr int PW = ProducerWarps<Loader>::value;
+  static constexpr int EW = EpiWarps<Epi>::value;
+  static constexpr int MMA_WARP = PW + EW;
+  static constexpr int THREADS = (MMA_WARP + 1) * 32;
+  static_assert(EW % 4 == 0, "epilogue warps must cover the 4 TMEM lane quarters equally");
+};
 constexpr int TC_TABLE_BYTES = 20480;              // loader lookup tables
 constexpr int TC_MAX_LAG = 8;
 
@@ -115,9 +136,10 @@ struct TcSmemLayout {
 };
 
 template <int BN, class Loader, class Epi>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Loader ld, const __grid_constant__ Epi epi, const TcShape shape) {
   using L = TcSmemLayout<BN>;
+  using R = TcRoles<Loader, Epi>;
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -139,19 +161,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], TC_EPI_WARPS * 32);
+      mbar_init(&tempty[i], R::EW * 32);
     }
     fence_barrier_init();
   }
-  if (warp == TC_MMA_WARP) tmem_alloc(tmem_base_slot, L::TMEM_COLS);
-  ld.init(table, threadIdx.x, TC_THREADS);
+  if (warp == R::MMA_WARP) tmem_alloc(tmem_base_slot, L::TMEM_COLS);
+  ld.init(table, threadIdx.x, R::THREADS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   const uint32_t smem_base = smem_u32(smem);
 
-  if (warp < TC_EPI_WARP0) {
+  if (warp < R::PW) {
     // ------------------------------------------------------------ producers
     if (Loader::PURE_TMA && threadIdx.x != 0) goto teardown;  // one thread issues every copy
     constexpr int LAG = L::LAG;
@@ -192,13 +214,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     cp_async_wait_all();
     fence_proxy_async();
     for (int i = 0; i < npending; ++i) mbar_arrive(&full[pending_stage[i]]);
-  } else if (warp < TC_MMA_WARP) {
+  } else if (warp < R::MMA_WARP) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter (warp % 4 == q)
-    const int half = (warp - TC_EPI_WARP0) >> 2;
-    constexpr int HALF_COLS = BN >= 32 ? BN / 2 : BN;
-    const int col_begin = half * HALF_COLS;
-    const int col_end = BN >= 32 ? col_begin + HALF_COLS : (half == 0 ? BN : 0);
+    const int grp = (warp - R::PW) >> 2;  // column group of this warp
+    constexpr int GROUPS = R::EW / 4;
+    constexpr int GCOLS = (BN / GROUPS) >= 16 ? BN / GROUPS : 16;  // multiple of 16
+    const int col_begin = grp * GCOLS;
+    const int col_end = col_begin + GCOLS < BN ? col_begin + GCOLS : BN;
     const int row_in_tile = q * 32 + lane;
     int lt = 0;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++lt) {
@@ -275,7 +298,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 teardown:
   tc_fence_before();
   __syncthreads();
-  if (warp == TC_MMA_WARP) {
+  if (warp == R::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc(tmem_base, L::TMEM_COLS);
   }
@@ -298,7 +321,7 @@ inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& sh
   int tiles = shape.m_tiles * shape.n_tiles * shape.splits;
   int grid = tiles < num_sms ? tiles : num_sms;
   if (grid < 1) grid = 1;
-  kern<<<grid, TC_THREADS, L::TOTAL, st>>>(ld, epi, shape);
+  kern<<<grid, TcRoles<Loader, Epi>::THREADS, L::TOTAL, st>>>(ld, epi, shape);
   return cudaGetLastError();
 }
 
