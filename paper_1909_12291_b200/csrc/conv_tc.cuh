@@ -465,6 +465,20 @@ struct WgradTcEpi {
 };
 
 // ------------------------------------------------------------------ dispatch
+// N-tile width: the smallest power of two >= n (16..256), halved while that
+// lowers the wave-quantised cost  ceil(tiles / #SMs) * (BN + 32)  (the +32
+// models the per-tile fixed cost: A loads, epilogue, pipeline ramp).
+inline int pick_bn(int m_tiles, int n, int num_sms) {
+  int bn = 16;
+  while (bn < n && bn < 256) bn *= 2;
+  auto cost = [&](int b) {
+    const long long tiles = (long long)m_tiles * ((n + b - 1) / b);
+    return ((tiles + num_sms - 1) / num_sms) * (long long)(b + 32);
+  };
+  while (bn > 64 && cost(bn / 2) < cost(bn)) bn /= 2;
+  return bn;
+}
+
 template <class Fn>
 inline int with_bn(int n, Fn&& fn) {
   if (n <= 16) return fn(std::integral_constant<int, 16>());
@@ -478,7 +492,7 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
                        int num_sms, cudaStream_t st) {
   const int M = g.n * g.oh * g.ow, K = g.k * g.k * g.c;
   if ((K / 8) * 4 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_fwd_tc: K=%d exceeds the chunk table", K);
-  return with_bn(g.co, [&](auto bn) {
+  return with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.co, num_sms), [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
     FwdTcEpi ep{y, bias, M, g.co, relu};
@@ -528,7 +542,7 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
       if (cl.ti == 0 || cl.tj == 0) continue;
       const int M = g.n * cl.hc * cl.wc, K = cl.ti * cl.tj * g.co;
       if ((K / 8) * 12 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_dgrad_tc: K=%d exceeds the chunk table", K);
-      int s = with_bn(g.c, [&](auto bn) {
+      int s = with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.c, num_sms), [&](auto bn) {
         constexpr int BN = decltype(bn)::value;
         TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
         const bf16* wcls = wt + dg_class_base(g.k, g.s, g.c, g.co, rh * g.s + rw);
@@ -561,12 +575,14 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
 }
 
 inline int conv_wgrad_splits(const ConvGeom& g, int n, int num_sms) {
+  // one wave: m_tiles * splits <= #SMs (a second, partial wave would double the
+  // kernel time for a few CTAs), at least 4 k-blocks per split
   const int Kf = g.k * g.k * g.c;
   const long long Mo = (long long)n * g.oh * g.ow;
   const int m_tiles = (Kf + TC_BM - 1) / TC_BM;
   const long long nkb = (Mo + TC_BK - 1) / TC_BK;
-  long long want = (num_sms + m_tiles - 1) / m_tiles;
-  if (want > nkb / 4) want = nkb / 4;  // at least 4 k-blocks per split
+  long long want = num_sms / m_tiles;
+  if (want > nkb / 4) want = nkb / 4;
   if (want > 128) want = 128;
   if (want < 1) want = 1;
   return (int)want;
