@@ -96,6 +96,12 @@ int ce_net_num_param_layers(const ce_net* net, int* count);
 /* param layer p: weights in reference layout (conv (o,c,kh,kw), dense (o,in)), bias (o) */
 int ce_net_set_params(ce_net* net, int p, const float* w, const float* b);
 int ce_net_get_params(ce_net* net, int p, float* w, float* b, float* vel_w, float* vel_b);
+/* param layer p: Kaiming-uniform U(-limit, limit) weights drawn on the device from the
+ * numpy PCG64 stream whose 128-bit state / increment are given (the state the
+ * reference's default_rng(seed) has when it reaches this layer, genome.py:313,
+ * nn.py:44-46); bit-exact to the host draw. Zero bias and velocities.           */
+int ce_net_init_uniform(ce_net* net, int p, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                        uint64_t inc_lo, double limit);
 /* retain raw parameter gradients of the next steps for ce_net_get_grads (off by default) */
 int ce_net_keep_grads(ce_net* net, int on);
 int ce_net_get_grads(ce_net* net, int p, float* gw, float* gb);

@@ -16,6 +16,7 @@
 #include "ops.cuh"
 #include "conv_tc.cuh"
 #include "dense_tc.cuh"
+#include "init.cuh"
 
 namespace ce {
 
@@ -780,6 +781,46 @@ int ce_net_set_params(ce_net* net, int p, const float* w, const float* b) {
     f32_to_bf16_pad_kernel<<<grid_for((size_t)l.out_units * l.in_pad), 256, 0, st>>>(l.W, l.out_units, l.in_units,
                                                                                       l.in_pad, l.Wbp);
   if (l.Wtbf) conv_wt_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.s, l.g.c, l.Wtbf);
+  CE_CHECK_LAUNCH();
+  CE_CUDA(cudaStreamSynchronize(st));
+  return CE_OK;
+}
+
+// Seeded Kaiming-uniform init on the device (init.cuh), bit-exact to the host draw.
+int ce_net_init_uniform(ce_net* net, int p, uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
+                        double limit) {
+  Layer* lp;
+  if (int s = param_layer(net, p, &lp)) return s;
+  Layer& l = *lp;
+  DevGuard dg(net->device);
+  cudaStream_t st = net->st;
+  InitLayout L{};
+  size_t count = host_w_count(l);
+  if (l.kind == CE_LAYER_CONV) {
+    L.kind = 1;
+    L.co = l.g.co;
+    L.cin = l.c_real;
+    L.k = l.g.k;
+    L.cp = l.g.c;
+  } else if (l.in_is_act) {
+    L.kind = 2;
+    L.cp = l.in_units / l.hw_in;
+    L.hw = l.hw_in;
+    L.in_ref = (long long)l.hw_in * l.c_real;
+    L.in_dev = l.in_units;
+  }
+  CE_CUDA(cudaMemsetAsync(l.W, 0, l.wn * 4, st));
+  const size_t nchunks = (count + kInitChunk - 1) / kInitChunk;
+  kaiming_uniform_kernel<<<grid_for(nchunks, 128), 128, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, count, limit, L, l.W);
+  CE_CHECK_LAUNCH();
+  CE_CUDA(cudaMemsetAsync(l.b, 0, l.bn * 4, st));
+  CE_CUDA(cudaMemsetAsync(l.VW, 0, l.wn * 4, st));
+  CE_CUDA(cudaMemsetAsync(l.Vb, 0, l.bn * 4, st));
+  if (l.Wbf) f32_to_bf16_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.wn, l.Wbf);
+  if (l.Wtbf) conv_wt_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.s, l.g.c, l.Wtbf);
+  if (l.Wbp)
+    f32_to_bf16_pad_kernel<<<grid_for((size_t)l.out_units * l.in_pad), 256, 0, st>>>(l.W, l.out_units, l.in_units,
+                                                                                      l.in_pad, l.Wbp);
   CE_CHECK_LAUNCH();
   CE_CUDA(cudaStreamSynchronize(st));
   return CE_OK;

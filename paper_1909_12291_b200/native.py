@@ -54,6 +54,7 @@ _SIGNATURES = {
     "ce_net_num_param_layers": ([_P, C.POINTER(C.c_int)], C.c_int),
     "ce_net_set_params": ([_P, C.c_int, _F, _F], C.c_int),
     "ce_net_get_params": ([_P, C.c_int, _F, _F, _F, _F], C.c_int),
+    "ce_net_init_uniform": ([_P, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double], C.c_int),
     "ce_net_keep_grads": ([_P, C.c_int], C.c_int),
     "ce_net_get_grads": ([_P, C.c_int, _F, _F], C.c_int),
     "ce_net_forward_host": ([_P, _F, C.c_int, _F], C.c_int),
@@ -217,6 +218,12 @@ class Net:
         w = np.ascontiguousarray(w, dtype=np.float32)
         b = np.ascontiguousarray(b, dtype=np.float32)
         check(load().ce_net_set_params(self._h, p, fptr(w), fptr(b)))
+
+    def init_uniform(self, p, state, inc, limit):
+        """Device Kaiming init from a PCG64 (state, inc) pair (128-bit ints)."""
+        m = (1 << 64) - 1
+        check(load().ce_net_init_uniform(self._h, p, (state >> 64) & m, state & m, (inc >> 64) & m, inc & m,
+                                         float(limit)))
 
     def get_params(self, p, w_shape, b_shape):
         w, b = np.empty(w_shape, np.float32), np.empty(b_shape, np.float32)

@@ -41,10 +41,11 @@ class DenseLayer:
     out_units: int
 
 
-def _kaiming(rng, shape, fan_in, dtype, chunk=1 << 26):
+def _kaiming(rng, shape, fan_in, dtype, chunk=1 << 26, limit=None):
     """rng.uniform(-l, l, size=shape).astype(dtype), drawn in chunks so giant
     heads never materialise a float64 copy (same stream, same values)."""
-    limit = np.sqrt(6.0 / fan_in)
+    if limit is None:
+        limit = np.sqrt(6.0 / fan_in)
     total = int(np.prod(shape))
     out = np.empty(total, dtype=dtype)
     for start in range(0, total, chunk):
@@ -54,16 +55,32 @@ def _kaiming(rng, shape, fan_in, dtype, chunk=1 << 26):
 
 
 class Network:
-    """Host description of an instantiated genome plus its device instance."""
+    """Host description of an instantiated genome plus its device instance.
 
-    def __init__(self, genome, input_shape, layers, weights, class_count=2):
+    Weights are "lazy" when built by instantiate(): only the PCG64 stream
+    position of each layer is kept, the device draws the values itself
+    (ce_net_init_uniform) and the host arrays are materialised on first access
+    to `weights` (same values, bit for bit)."""
+
+    def __init__(self, genome, input_shape, layers, weights, class_count=2, streams=None):
         self.genome = genome
         self.input_shape = tuple(input_shape)
         self.layers = layers            # ConvLayer / PoolLayer / DenseLayer in execution order
-        self.weights = weights          # [(W, b)] reference layout, parameterised layers in order
+        self._weights = weights         # [(W, b)] reference layout, or None while lazy
+        self.streams = streams          # [(state, inc, limit, shape, dtype)] per parameterised layer
         self.class_count = class_count
         self._dev = None
         self._dev_key = None
+
+    @property
+    def weights(self):
+        if self._weights is None:
+            self._weights = [_draw_layer(*st) for st in self.streams]
+        return self._weights
+
+    @weights.setter
+    def weights(self, value):
+        self._weights = value
 
     # -- accounting (evaluator.py:116-136) ---------------------------------
     def parameters(self):
@@ -117,8 +134,12 @@ class Network:
         self.release()
         net = native.Net(self.native_layers(), self.input_shape, max_batch, device, precision)
         try:
-            for p, (w, b) in enumerate(self.weights):
-                net.set_params(p, w, b)
+            if self._weights is None:
+                for p, (state, inc, limit, _, _) in enumerate(self.streams):
+                    net.init_uniform(p, state, inc, limit)
+            else:
+                for p, (w, b) in enumerate(self.weights):
+                    net.set_params(p, w, b)
         except Exception:
             net.close()
             raise
@@ -173,17 +194,38 @@ def build_layers(genome, input_shape):
     return layers
 
 
-def instantiate(genome, input_shape, seed, dtype=np.float32):
-    """Build the network for `genome` with seeded Kaiming-uniform weights."""
+def _draw_layer(state, inc, limit, shape, dtype):
+    """Host draw of one layer's Kaiming weights from a recorded PCG64 position."""
+    bg = np.random.PCG64()
+    bg.state = {"bit_generator": "PCG64", "state": {"state": state, "inc": inc}, "has_uint32": 0, "uinteger": 0}
+    rng = np.random.Generator(bg)
+    w = _kaiming(rng, shape, None, dtype, limit=limit)
+    return w, np.zeros(shape[0], dtype=dtype)
+
+
+def instantiate(genome, input_shape, seed, dtype=np.float32, lazy=True):
+    """Build the network for `genome` with seeded Kaiming-uniform weights.
+
+    Draw order and values follow genome.py:309-335 / nn.py:44-46 exactly. With
+    lazy=True the host only records where each layer's draws start in the
+    PCG64 stream (and advances past them); the values are produced on the
+    device, or on the host when `weights` is first read."""
     layers = build_layers(genome, tuple(input_shape))
     rng = np.random.default_rng(seed)
-    weights = []
+    streams = []
     for layer in layers:
         if isinstance(layer, ConvLayer):
             fan_in = layer.in_channels * layer.kernel ** 2
-            w = _kaiming(rng, (layer.out_channels, layer.in_channels, layer.kernel, layer.kernel), fan_in, dtype)
-            weights.append((w, np.zeros(layer.out_channels, dtype=dtype)))
+            shape = (layer.out_channels, layer.in_channels, layer.kernel, layer.kernel)
         elif isinstance(layer, DenseLayer):
-            w = _kaiming(rng, (layer.out_units, layer.in_units), layer.in_units, dtype)
-            weights.append((w, np.zeros(layer.out_units, dtype=dtype)))
-    return Network(genome, input_shape, layers, weights)
+            fan_in = layer.in_units
+            shape = (layer.out_units, layer.in_units)
+        else:
+            continue
+        st = rng.bit_generator.state["state"]
+        streams.append((st["state"], st["inc"], float(np.sqrt(6.0 / fan_in)), shape, dtype))
+        rng.bit_generator.advance(int(np.prod(shape)))
+    net = Network(genome, input_shape, layers, None, streams=streams)
+    if not lazy:
+        net.weights  # materialise now
+    return net

@@ -93,3 +93,19 @@ def test_sgd_bit_exact_fp32():
         assert rel(nw, oracle.params[0][0]) < 1e-6
     finally:
         net.release()
+
+
+@pytest.mark.parametrize("name,text,shape", CASES, ids=[c[0] for c in CASES])
+def test_device_init_bit_exact(name, text, shape):
+    """ce_net_init_uniform (device PCG64 jump-ahead) == the host Kaiming draw, bit for bit."""
+    genome = case_genome(text)
+    lazy = instantiate(genome, shape, seed=17)            # weights drawn on the device
+    dev = lazy.to_device(0, "bf16", max_batch=4)
+    host = instantiate(genome, shape, seed=17, lazy=False)  # weights drawn by numpy
+    try:
+        for p, (w, b) in enumerate(host.weights):
+            dw, db, vw, vb = dev.get_params(p, w.shape, b.shape)
+            np.testing.assert_array_equal(dw, w)
+            assert not db.any() and not vw.any() and not vb.any()
+    finally:
+        lazy.release()
