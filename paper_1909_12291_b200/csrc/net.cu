@@ -104,7 +104,8 @@ struct ce_net {
   size_t gbytes = 0;
   float* ws = nullptr;
   size_t ws_bytes = 0;
-  int* d_step = nullptr;
+  int* d_step = nullptr;   // [0] step counter, [1] non-finite flag
+  int* h_flags = nullptr;  // pinned: non-finite flag snapshots of in-flight chunks
   float* d_losses = nullptr;
   int losses_cap = 0;
   int32_t* d_perm = nullptr;
@@ -403,7 +404,7 @@ int enqueue_step(ce_net* net, int n, float lr, float mu) {
   {
     Prof pf(net, P_LOSS, 0.0, 16.0 * n * net->classes);
     xent_kernel<<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes,
-                                          (float*)net->gbuf[0], net->d_losses, net->d_step);
+                                          (float*)net->gbuf[0], net->d_losses, net->d_step, net->d_step + 1);
     CE_CHECK_LAUNCH();
   }
   return enqueue_backward<T>(net, n, lr, mu);
@@ -537,6 +538,7 @@ int ce_net_destroy(ce_net* net) {
   if (!net) return CE_OK;
   DevGuard dg(net->device);
   cudaStreamSynchronize(net->st);
+  if (net->h_flags) cudaFreeHost(net->h_flags);
   for (void* p : net->allocs) cudaFreeAsync(p, net->st);
   cudaStreamSynchronize(net->st);
   cudaStreamDestroy(net->st);
@@ -963,7 +965,11 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
     net->perm_cap = pn;
   }
   CE_CUDA(cudaMemcpyAsync(net->d_perm, perm, pn * 4, cudaMemcpyHostToDevice, st));
-  CE_CUDA(cudaMemsetAsync(net->d_step, 0, 4, st));
+  CE_CUDA(cudaMemsetAsync(net->d_step, 0, 8, st));
+  CE_CUDA(cudaMemsetAsync(net->d_losses, 0, (size_t)steps * 4, st));
+  if (!net->h_flags) {
+    CE_CUDA(cudaHostAlloc((void**)&net->h_flags, 4 * sizeof(int), cudaHostAllocDefault));
+  }
   // capture one step (profiling runs eagerly so each launch can be bracketed)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -984,24 +990,45 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   }
   cudaGetLastError();
   net->acc = 0;
-  cudaEvent_t e0, e1;
+  cudaEvent_t e0, e1, chunk_ev[2];
   CE_CUDA(cudaEventCreate(&e0));
   CE_CUDA(cudaEventCreate(&e1));
+  CE_CUDA(cudaEventCreateWithFlags(&chunk_ev[0], cudaEventDisableTiming));
+  CE_CUDA(cudaEventCreateWithFlags(&chunk_ev[1], cudaEventDisableTiming));
   CE_CUDA(cudaEventRecord(e0, st));
-  for (int i = 0; i < steps; ++i) {
-    if (graphed) {
-      CE_CUDA(cudaGraphLaunch(exec, st));
-    } else {
-      if (int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true)) return s;
-      if (int s = step_any(net, batch, lr, momentum)) return s;
+  // Replay in chunks; after each chunk snapshot the device non-finite flag. With
+  // one chunk in flight ahead, a diverged candidate stops within two chunks
+  // (the reference stops at the first non-finite loss, evaluator.py:168-170).
+  const int chunk = 16;
+  int launched = 0, nchunk = 0;
+  while (launched < steps) {
+    const int todo = std::min(chunk, steps - launched);
+    for (int i = 0; i < todo; ++i) {
+      if (graphed) {
+        CE_CUDA(cudaGraphLaunch(exec, st));
+      } else {
+        if (int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true)) return s;
+        if (int s = step_any(net, batch, lr, momentum)) return s;
+      }
     }
+    launched += todo;
+    const int slot = nchunk & 1;
+    CE_CUDA(cudaMemcpyAsync(net->h_flags + slot, net->d_step + 1, 4, cudaMemcpyDeviceToHost, st));
+    CE_CUDA(cudaEventRecord(chunk_ev[slot], st));
+    if (nchunk >= 1) {
+      CE_CUDA(cudaEventSynchronize(chunk_ev[slot ^ 1]));
+      if (net->h_flags[slot ^ 1]) break;
+    }
+    ++nchunk;
   }
-  g_launches += graphed ? per_step * steps : net->acc;
+  g_launches += graphed ? per_step * launched : net->acc;
   CE_CUDA(cudaEventRecord(e1, st));
   CE_CUDA(cudaMemcpyAsync(losses, net->d_losses, (size_t)steps * 4, cudaMemcpyDeviceToHost, st));
   cudaError_t se = cudaStreamSynchronize(st);
   if (exec) cudaGraphExecDestroy(exec);
   if (net->prof_on) prof_collect(net);
+  cudaEventDestroy(chunk_ev[0]);
+  cudaEventDestroy(chunk_ev[1]);
   if (se != cudaSuccess) return fail(CE_ECUDA, "train loop: %s", cudaGetErrorString(se));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);

@@ -294,7 +294,8 @@ __global__ void dense_reduce_kernel(const float* __restrict__ part, int splits, 
 // loss = -mean(logp[label]); grad = (softmax - onehot) / B.
 // Writes losses[*step] and advances the step counter (end of the step).
 __global__ void xent_kernel(const float* __restrict__ logits, const int32_t* __restrict__ y, int B, int K,
-                            float* __restrict__ grad, float* __restrict__ losses, int* __restrict__ step_ctr) {
+                            float* __restrict__ grad, float* __restrict__ losses, int* __restrict__ step_ctr,
+                            int* __restrict__ nonfinite) {
   __shared__ double red[1024];
   const int b = threadIdx.x;
   double lp = 0.0;
@@ -324,7 +325,9 @@ __global__ void xent_kernel(const float* __restrict__ logits, const int32_t* __r
   }
   if (threadIdx.x == 0) {
     const int step = *step_ctr;
-    losses[step] = (float)(-red[0] / B);
+    const float loss = (float)(-red[0] / B);
+    losses[step] = loss;
+    if (nonfinite && !isfinite(loss)) *nonfinite = 1;  // host stops replaying (evaluator.py:168-170)
     *step_ctr = step + 1;
   }
 }
