@@ -156,6 +156,27 @@ struct DevGuard {
 
 inline size_t act_bytes(const ce_net* net) { return net->prec == CE_PREC_FP32 ? 4 : 2; }
 
+// Two pinned ints per ce_train call for the non-finite flag snapshots, carved
+// from one process-wide pinned block (cudaHostAlloc per net costs milliseconds).
+int* pinned_flag_slots() {
+  static std::atomic<unsigned> next{0};
+  static int* block = nullptr;
+  static std::atomic<int> ready{0};
+  constexpr unsigned kSlots = 4096;
+  if (!ready.load()) {
+    static std::atomic_flag lock = ATOMIC_FLAG_INIT;
+    while (lock.test_and_set()) {
+    }
+    if (!ready.load()) {
+      if (cudaHostAlloc((void**)&block, kSlots * 2 * sizeof(int), cudaHostAllocPortable) != cudaSuccess) block = nullptr;
+      ready.store(1);
+    }
+    lock.clear();
+  }
+  if (!block) return nullptr;
+  return block + 2 * (next.fetch_add(1) % kSlots);
+}
+
 // The stream-ordered pool returns freed memory to the OS at every sync by
 // default; candidates come and go every few ms, so keep it cached instead.
 void keep_pool_memory(int device) {
@@ -538,7 +559,6 @@ int ce_net_destroy(ce_net* net) {
   if (!net) return CE_OK;
   DevGuard dg(net->device);
   cudaStreamSynchronize(net->st);
-  if (net->h_flags) cudaFreeHost(net->h_flags);
   for (void* p : net->allocs) cudaFreeAsync(p, net->st);
   cudaStreamSynchronize(net->st);
   cudaStreamDestroy(net->st);
@@ -968,7 +988,8 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   CE_CUDA(cudaMemsetAsync(net->d_step, 0, 8, st));
   CE_CUDA(cudaMemsetAsync(net->d_losses, 0, (size_t)steps * 4, st));
   if (!net->h_flags) {
-    CE_CUDA(cudaHostAlloc((void**)&net->h_flags, 4 * sizeof(int), cudaHostAllocDefault));
+    net->h_flags = pinned_flag_slots();
+    if (!net->h_flags) return fail(CE_ENOMEM, "pinned flag pool allocation failed");
   }
   // capture one step (profiling runs eagerly so each launch can be bracketed)
   cudaGraph_t graph = nullptr;
