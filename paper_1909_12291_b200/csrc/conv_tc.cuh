@@ -71,7 +71,7 @@ inline bool make_tmap_mn64(CUtensorMap* map, const bf16* base, int krows, int mn
 // convolution with kernel k and stride s: `pixels` output pixels x 64 channels
 // per copy (128 B rows, SWIZZLE_128B), receptive-field origins traversed in
 // (n, p, q) order with stride s (bounding box shrunk by k-1 on the far side).
-inline bool make_tmap_im2col(CUtensorMap* map, const bf16* x, const ConvGeom& g, int pixels) {
+inline bool make_tmap_im2col(CUtensorMap* map, const bf16* x, const ConvGeom& g, int pixels, int cpp = 64) {
   static PFN_cuTensorMapEncodeIm2col_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -84,8 +84,9 @@ inline bool make_tmap_im2col(CUtensorMap* map, const bf16* x, const ConvGeom& g,
   int lower[2] = {0, 0};
   int upper[2] = {-(g.k - 1), -(g.k - 1)};
   cuuint32_t estr[4] = {1, (cuuint32_t)g.s, (cuuint32_t)g.s, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)x, dims, strides, lower, upper, 64,
-                      (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)x, dims, strides, lower, upper,
+                      (cuuint32_t)cpp, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      cpp == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   // driver <= 13.1 workaround (as in CUTLASS): small tensors must not set bit 21 of word 1
@@ -109,9 +110,12 @@ inline bool im2col_disabled() {
 // output pixel's receptive-field origin: (i*W + j)*C + c0.
 template <int MODE>
 struct FwdTcLoader {
-  static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2;
+  // MODE 0: cp.async gather A + cp.async B; 1: gather A + TMA B;
+  //      2: TMA im2col A (64-channel slabs, SW128) + TMA B;
+  //      3: TMA im2col A in 8-channel chunks (C < 64, interleaved layout) + TMA B
+  static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2, NARROW = MODE == 3;
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL;
+  static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL || NARROW;
   CUtensorMap wmap;  // B operand (weights) when TMA_B
   CUtensorMap xmap;  // im2col view of x when IM2COL
   const bf16* x;
@@ -120,7 +124,7 @@ struct FwdTcLoader {
   int K, M, BN;
   FastDiv d_ow, d_oh;
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
-    if (IM2COL) return;
+    if (IM2COL || NARROW) return;
     int* xoff = (int*)table;
     for (int k8 = tid; k8 < K / 8; k8 += nthreads) {
       const int kk = k8 * 8, tap = kk / g.c, c0 = kk - tap * g.c;
@@ -140,6 +144,27 @@ struct FwdTcLoader {
       d_oh.divmod(t, n, p);
       mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
       tma_load_im2col_4d(sA, &xmap, c0, (int)q * g.s, (int)p * g.s, (int)n, (uint16_t)j, (uint16_t)i, full);
+      tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+      return;
+    }
+    if (NARROW) {  // one thread: 8 im2col copies of 128 pixels x 8 channels (one per 16-byte K chunk)
+      uint32_t q, p, n, t;
+      d_ow.divmod((uint32_t)c.m0, t, q);
+      d_oh.divmod(t, n, p);
+      mbar_expect_tx(full, (uint32_t)(8 * TC_BM * 16 + BN * 128));
+#pragma unroll 1
+      for (int kc = 0; kc < 8; ++kc) {
+        const int kk = kb * TC_BK + kc * 8;
+        int c0 = g.c, i = 0, j = 0;  // past K: a fully out-of-bounds copy zero-fills the chunk
+        if (kk < K) {
+          const int tap = kk / g.c;
+          c0 = kk - tap * g.c;
+          i = tap / g.k;
+          j = tap - i * g.k;
+        }
+        tma_load_im2col_4d(sA + kmajor_off(TC_BM, 0, kc), &xmap, c0, (int)q * g.s, (int)p * g.s, (int)n,
+                           (uint16_t)j, (uint16_t)i, full);
+      }
       tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
       return;
     }
@@ -216,9 +241,10 @@ struct DgradClass {
 
 template <int MODE>
 struct DgradTcLoader {
-  static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2;
+  // MODE as FwdTcLoader (3 = 8-channel im2col chunks for C_out < 64)
+  static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2, NARROW = MODE == 3;
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL;
+  static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL || NARROW;
   CUtensorMap wmap;  // class block [c][K] when TMA_B
   CUtensorMap dmap;  // im2col view of dY for this class when IM2COL
   const bf16* dy;
@@ -228,7 +254,7 @@ struct DgradTcLoader {
   int K, M, BN;    // K = ti*tj*co, M = n*hc*wc
   FastDiv d_wc, d_hc;
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
-    if (IM2COL) return;
+    if (IM2COL || NARROW) return;
     const int nk8 = K / 8;
     int* doff = (int*)table;
     int* dab = doff + nk8;
@@ -257,6 +283,27 @@ struct DgradTcLoader {
       mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
       tma_load_im2col_4d(sA, &dmap, o0, (int)ww - (cl.tj - 1), (int)hh - (cl.ti - 1), (int)n, (uint16_t)bp,
                          (uint16_t)ap, full);
+      tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+      return;
+    }
+    if (NARROW) {
+      uint32_t ww, hh, n, t;
+      d_wc.divmod((uint32_t)c.m0, t, ww);
+      d_hc.divmod(t, n, hh);
+      mbar_expect_tx(full, (uint32_t)(8 * TC_BM * 16 + BN * 128));
+#pragma unroll 1
+      for (int kc = 0; kc < 8; ++kc) {
+        const int kk = kb * TC_BK + kc * 8;
+        int o0 = g.co, ap = 0, bp = 0;  // past K: out-of-bounds copy zero-fills the chunk
+        if (kk < K) {
+          const int tap = kk / g.co;
+          o0 = kk - tap * g.co;
+          ap = tap / cl.tj;
+          bp = tap - ap * cl.tj;
+        }
+        tma_load_im2col_4d(sA + kmajor_off(TC_BM, 0, kc), &dmap, o0, (int)ww - (cl.tj - 1), (int)hh - (cl.ti - 1),
+                           (int)n, (uint16_t)bp, (uint16_t)ap, full);
+      }
       tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
       return;
     }
@@ -306,7 +353,8 @@ struct DgradTcLoader {
 // im2col view of dY for one dgrad residue class: a stride-1 "full" convolution
 // with a ti x tj kernel, i.e. padding ti-1 / tj-1 on the near side and a far
 // edge that yields exactly hc x wc receptive-field origins.
-inline bool make_tmap_im2col_dgrad(CUtensorMap* map, const bf16* dy, const ConvGeom& g, const DgradClass& cl) {
+inline bool make_tmap_im2col_dgrad(CUtensorMap* map, const bf16* dy, const ConvGeom& g, const DgradClass& cl,
+                                   int cpp = 64) {
   static PFN_cuTensorMapEncodeIm2col_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -321,9 +369,10 @@ inline bool make_tmap_im2col_dgrad(CUtensorMap* map, const bf16* dy, const ConvG
   if (lower[0] < -128 || lower[1] < -128 || upper[0] < -128 || upper[1] < -128 || upper[0] > 127 || upper[1] > 127)
     return false;
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)dy, dims, strides, lower, upper, 64, TC_BM, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)dy, dims, strides, lower, upper,
+                      (cuuint32_t)cpp, TC_BM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      cpp == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   int drv = 0;
   cudaDriverGetVersion(&drv);
@@ -503,11 +552,16 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
       ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
     };
     FwdTcLoader<2> ld2{};
+    FwdTcLoader<3> ld3{};
     FwdTcLoader<1> ld1{};
     if (tma && g.c % 64 == 0 && !im2col_disabled() && make_tmap_kmajor(&ld2.wmap, w, g.co, K, BN) &&
         make_tmap_im2col(&ld2.xmap, x, g, TC_BM)) {
       fill(ld2);
       e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
+    } else if (tma && !im2col_disabled() && make_tmap_kmajor(&ld3.wmap, w, g.co, K, BN) &&
+               make_tmap_im2col(&ld3.xmap, x, g, TC_BM, 8)) {
+      fill(ld3);
+      e = tc_launch<BN>(ld3, ep, sh, num_sms, st);
     } else if (tma && make_tmap_kmajor(&ld1.wmap, w, g.co, K, BN)) {
       fill(ld1);
       e = tc_launch<BN>(ld1, ep, sh, num_sms, st);
@@ -554,11 +608,16 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
           ld.d_wc = FastDiv(cl.wc); ld.d_hc = FastDiv(cl.hc);
         };
         DgradTcLoader<2> ld2{};
+        DgradTcLoader<3> ld3{};
         DgradTcLoader<1> ld1{};
         if (tma && g.co % 64 == 0 && !im2col_disabled() && make_tmap_kmajor(&ld2.wmap, wcls, g.c, K, BN) &&
             make_tmap_im2col_dgrad(&ld2.dmap, dy, g, cl)) {
           fill(ld2);
           e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
+        } else if (tma && !im2col_disabled() && make_tmap_kmajor(&ld3.wmap, wcls, g.c, K, BN) &&
+                   make_tmap_im2col_dgrad(&ld3.dmap, dy, g, cl, 8)) {
+          fill(ld3);
+          e = tc_launch<BN>(ld3, ep, sh, num_sms, st);
         } else if (tma && make_tmap_kmajor(&ld1.wmap, wcls, g.c, K, BN)) {
           fill(ld1);
           e = tc_launch<BN>(ld1, ep, sh, num_sms, st);

@@ -15,27 +15,28 @@ namespace ce {
 // consumes each result. 64x64 tile, BK=16, 256 threads, 4x4 outputs per thread.
 constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
 
-template <class AF, class BF, class EP>
+template <int TM, class AF, class BF, class EP>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(const AF A, const BF B, const EP E, int M, int N, int K,
                                                        int kchunk) {
-  __shared__ float As[SG_BK][SG_BM + 4];
+  constexpr int BM = 16 * TM;  // TM rows per thread: 64-row tiles, or 32 for skinny M (batch rows)
+  __shared__ float As[SG_BK][BM + 4];
   __shared__ float Bs[SG_BK][SG_BN + 4];
-  const int m0 = blockIdx.x * SG_BM, n0 = blockIdx.y * SG_BN;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * SG_BN;
   const int kbeg = blockIdx.z * kchunk;
   const int kend = min(K, kbeg + kchunk);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][4];
+  float acc[TM][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   for (int k0 = kbeg; k0 < kend; k0 += SG_BK) {
 #pragma unroll
-    for (int e = threadIdx.x; e < SG_BM * SG_BK; e += 256) {
+    for (int e = threadIdx.x; e < BM * SG_BK; e += 256) {
       int mm, kk;
       if (AF::M_FAST) {
-        mm = e % SG_BM;
-        kk = e / SG_BM;
+        mm = e % BM;
+        kk = e / BM;
       } else {
         kk = e % SG_BK;
         mm = e / SG_BK;
@@ -59,21 +60,21 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const AF A, const BF B, 
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < SG_BK; ++kk) {
-      float a[4], b[4];
+      float a[TM], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty * 4 + i;
+  for (int i = 0; i < TM; ++i) {
+    const int m = m0 + ty * TM + i;
     if (m >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -90,8 +91,13 @@ inline void simt_gemm(const AF& A, const BF& B, const EP& E, int M, int N, int K
   kchunk = cdiv(kchunk, SG_BK) * SG_BK;
   splits = cdiv(K, kchunk);
   if (splits < 1) splits = 1;
-  dim3 grid(cdiv(M, SG_BM), cdiv(N, SG_BN), splits);
-  simt_gemm_kernel<<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
+  if (M <= 32) {
+    dim3 grid(cdiv(M, 32), cdiv(N, SG_BN), splits);
+    simt_gemm_kernel<2><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
+  } else {
+    dim3 grid(cdiv(M, SG_BM), cdiv(N, SG_BN), splits);
+    simt_gemm_kernel<4><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
+  }
 }
 
 // Number of K splits used by simt_gemm for a requested split count.
