@@ -104,6 +104,12 @@ inline bool im2col_disabled() {
   const char* e = getenv("CE_DISABLE_IM2COL");
   return e && e[0] == '1';
 }
+// 8-channel im2col copies (C < 64) measured slower than the cp.async gather
+// (16-byte TMA boxes); opt-in only.
+inline bool narrow_im2col_enabled() {
+  const char* e = getenv("CE_NARROW_IM2COL");
+  return e && e[0] == '1';
+}
 
 // ------------------------------------------------------------------ forward
 // table: xoff[k8] = im2col offset of K chunk k8 = (tap, c0) relative to the
@@ -558,7 +564,7 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
         make_tmap_im2col(&ld2.xmap, x, g, TC_BM)) {
       fill(ld2);
       e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
-    } else if (tma && !im2col_disabled() && make_tmap_kmajor(&ld3.wmap, w, g.co, K, BN) &&
+    } else if (tma && narrow_im2col_enabled() && make_tmap_kmajor(&ld3.wmap, w, g.co, K, BN) &&
                make_tmap_im2col(&ld3.xmap, x, g, TC_BM, 8)) {
       fill(ld3);
       e = tc_launch<BN>(ld3, ep, sh, num_sms, st);
@@ -614,7 +620,7 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
             make_tmap_im2col_dgrad(&ld2.dmap, dy, g, cl)) {
           fill(ld2);
           e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
-        } else if (tma && !im2col_disabled() && make_tmap_kmajor(&ld3.wmap, wcls, g.c, K, BN) &&
+        } else if (tma && narrow_im2col_enabled() && make_tmap_kmajor(&ld3.wmap, wcls, g.c, K, BN) &&
                    make_tmap_im2col_dgrad(&ld3.dmap, dy, g, cl, 8)) {
           fill(ld3);
           e = tc_launch<BN>(ld3, ep, sh, num_sms, st);
