@@ -122,7 +122,7 @@ int ce_conv_wgrad(const ce_conv_desc* d, const void* x, const void* dy, float* d
   const int bsplits = tc ? colsum((const bf16*)dy, Mo, g.co, bpart, st) : colsum((const float*)dy, Mo, g.co, bpart, st);
   conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(part, splits, g.co, K, g.c, g.k, g.s, nullptr, nullptr,
                                                                dw, nullptr, nullptr, 0.f, 0.f);
-  bias_sgd_kernel<<<cdiv(g.co, 256), 256, 0, st>>>(bpart, bsplits, g.co, nullptr, nullptr, db, 0.f, 0.f);
+  launch_bias_sgd(bpart, bsplits, g.co, nullptr, nullptr, db, 0.f, 0.f, st);
   CE_CHECK_LAUNCH();
   return CE_OK;
 }

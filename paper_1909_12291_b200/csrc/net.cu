@@ -287,7 +287,7 @@ int enqueue_forward(ce_net* net, int n) {
         else
           simt_gemm(DenseXA<float>{(const float*)in, K}, DenseWB{l.W, K}, pe, B, O, K, splits, st);
       }
-      dense_reduce_kernel<<<grid_for((size_t)B * O), 256, 0, st>>>(net->ws, splits, B, O, l.b, (float*)l.out);
+      launch_dense_reduce(net->ws, splits, B, O, l.b, (float*)l.out, st);
     }
     CE_CHECK_LAUNCH();
     in = l.out;
@@ -358,7 +358,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       }
       float* bpart = net->ws;
       int bs = colsum(g, B, O, bpart, st);
-      bias_sgd_kernel<<<cdiv(O, 256), 256, 0, st>>>(bpart, bs, O, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
+      launch_bias_sgd(bpart, bs, O, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu, st);
       CE_CHECK_LAUNCH();
     } else if (l.kind == CE_LAYER_CONV) {
       ConvGeom g = l.g;
@@ -399,7 +399,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       int bsplits = colsum(dy, Mo, g.co, bpart, st);
       conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(net->ws, splits, g.co, K, g.c, g.k, g.s, l.W, l.VW,
                                                                    keep ? l.GW : nullptr, l.Wbf, l.Wtbf, lr, mu);
-      bias_sgd_kernel<<<cdiv(g.co, 256), 256, 0, st>>>(bpart, bsplits, g.co, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu);
+      launch_bias_sgd(bpart, bsplits, g.co, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu, st);
       CE_CHECK_LAUNCH();
     } else {  // pool
       if (l.need_dx) {

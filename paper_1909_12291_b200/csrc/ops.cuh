@@ -8,6 +8,13 @@
 
 namespace ce {
 
+inline int grid_for(size_t n, int threads = 256) {
+  size_t g = (n + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
 // ---------------------------------------------------------------- input
 // x[b][y][x][cp] = cp < C ? pix[idx[b]][cp][y][x] / 255 : 0      (data.py:65-66)
 // idx source: perm[epoch*n_perm + bi*B + b] with (epoch, bi) from the device
@@ -223,13 +230,13 @@ __global__ void colsum_partial_kernel(const T* __restrict__ dy, int M, int N, in
   }
 }
 
-constexpr int kColsumMaxSplits = 512;
+constexpr int kColsumMaxSplits = 256;
 
 // launches the column sum; returns the number of partial rows written
 template <class T>
 inline int colsum(const T* dy, int M, int N, float* part, cudaStream_t st) {
   if (N % 8 == 0 && N <= 2048) {
-    int rows = std::max(64, cdiv(M, kColsumMaxSplits));
+    int rows = std::max(256, cdiv(M, kColsumMaxSplits));
     int blocks = cdiv(M, rows);
     colsum8_kernel<T><<<blocks, 256, 0, st>>>(dy, M, N, rows, part);
     return blocks;
@@ -263,13 +270,25 @@ __global__ void conv_sgd_kernel(const float* __restrict__ part, int splits, int 
   }
 }
 
-// bias: g = sum_split part[split][o]
+// Fixed-order warp sum of part[s][stride * s + off] over s in [0, splits):
+// lane l adds s = l, l+32, ... then a fixed xor tree (deterministic).
+__device__ __forceinline__ float warp_sum_splits(const float* __restrict__ part, int splits, size_t stride,
+                                                 size_t off) {
+  const int lane = threadIdx.x & 31;
+  float acc = 0.f;
+  for (int s = lane; s < splits; s += 32) acc += part[(size_t)s * stride + off];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// bias: g = sum_split part[split][o]; one warp per output channel
 __global__ void bias_sgd_kernel(const float* __restrict__ part, int splits, int n, float* __restrict__ b,
                                 float* __restrict__ vel, float* __restrict__ gb, float lr, float mu) {
-  int o = blockIdx.x * blockDim.x + threadIdx.x;
+  const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (o >= n) return;
-  float g = 0.f;
-  for (int s = 0; s < splits; ++s) g += part[(size_t)s * n + o];
+  const float g = warp_sum_splits(part, splits, n, o);
+  if ((threadIdx.x & 31) != 0) return;
   if (gb) gb[o] = g;
   if (!b) return;
   float bv = b[o], vv = vel[o];
@@ -277,16 +296,35 @@ __global__ void bias_sgd_kernel(const float* __restrict__ part, int splits, int 
   b[o] = bv;
   vel[o] = vv;
 }
+inline void launch_bias_sgd(const float* part, int splits, int n, float* b, float* vel, float* gb, float lr, float mu,
+                            cudaStream_t st) {
+  bias_sgd_kernel<<<cdiv(n, 8), 256, 0, st>>>(part, splits, n, b, vel, gb, lr, mu);
+}
 
 // dense forward reduce: y[b][o] = bias[o] + sum_split part[split][b][o]
 __global__ void dense_reduce_kernel(const float* __restrict__ part, int splits, int B, int out,
                                     const float* __restrict__ bias, float* __restrict__ y) {
-  size_t total = (size_t)B * out;
+  const size_t total = (size_t)B * out;
+  if (splits >= 16) {  // one warp per output element
+    const size_t e = blockIdx.x * (size_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (e >= total) return;
+    const float acc = warp_sum_splits(part, splits, total, e);
+    if ((threadIdx.x & 31) == 0) y[e] = acc + bias[e % out];
+    return;
+  }
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
     for (int s = 0; s < splits; ++s) acc += part[(size_t)s * total + e];
     y[e] = acc + bias[e % out];
   }
+}
+inline void launch_dense_reduce(const float* part, int splits, int B, int out, const float* bias, float* y,
+                                cudaStream_t st) {
+  const size_t total = (size_t)B * out;
+  if (splits >= 16)
+    dense_reduce_kernel<<<(unsigned)((total + 7) / 8), 256, 0, st>>>(part, splits, B, out, bias, y);
+  else
+    dense_reduce_kernel<<<grid_for(total), 256, 0, st>>>(part, splits, B, out, bias, y);
 }
 
 // ---------------------------------------------------------------- loss
@@ -441,11 +479,5 @@ __global__ void transpose_w_bf16_kernel(const bf16* __restrict__ w, int co, int 
   }
 }
 
-inline int grid_for(size_t n, int threads = 256) {
-  size_t g = (n + threads - 1) / threads;
-  if (g > 148 * 16) g = 148 * 16;
-  if (g < 1) g = 1;
-  return (int)g;
-}
 
 }  // namespace ce
