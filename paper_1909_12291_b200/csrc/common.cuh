@@ -36,6 +36,26 @@ __device__ __forceinline__ void stf<bf16>(bf16* p, size_t i, float v) {
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// Division by a runtime-invariant divisor d (1 <= d < 2^31) for 0 <= n < 2^31:
+// q = (n * M) >> (32 + l), M = ceil(2^(32+l) / d), l = ceil(log2 d).
+struct FastDiv {
+  uint64_t mul;
+  uint32_t shift, d;
+  FastDiv() = default;
+  __host__ __device__ explicit FastDiv(uint32_t div) : d(div) {
+    uint32_t l = 0;
+    while ((1ull << l) < div) ++l;
+    shift = 32 + l;
+    mul = ((1ull << shift) + div - 1) / div;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (uint32_t)(((uint64_t)n * mul) >> shift); }
+  __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
+    q = div(n);
+    r = n - q * d;
+  }
+};
+
+
 // Thread-local last error message (ce_last_error).
 void set_error(const char* fmt, ...);
 int fail(int status, const char* fmt, ...);

@@ -71,7 +71,7 @@ int ce_conv_fwd(const ce_conv_desc* d, const void* x, const void* w, const float
     if (conv_tc_enabled()) return conv_fwd_tc(g, (const bf16*)x, (const bf16*)w, bias, relu, (bf16*)y, sms(), st);
     return fail(CE_EINVAL, "bf16 kernel-level conv requires the tensor-core path");
   }
-  simt_gemm(FwdA<float>{(const float*)x, g}, FwdB{(const float*)w, K}, FwdEpi<float>{(float*)y, bias, g.co, relu != 0},
+  simt_gemm(make_fwd_a((const float*)x, g), FwdB{(const float*)w, K}, FwdEpi<float>{(float*)y, bias, g.co, relu != 0},
             M, g.co, K, 1, st);
   CE_CHECK_LAUNCH();
   return CE_OK;
@@ -93,7 +93,7 @@ int ce_conv_dgrad(const ce_conv_desc* d, const void* dy, const void* w, const vo
     CE_CHECK_LAUNCH();
     return conv_dgrad_tc(g, (const bf16*)dy, wt, (const bf16*)mask, (bf16*)dx, sms(), st);
   }
-  simt_gemm(DgradA<float>{(const float*)dy, g}, DgradB{(const float*)w, g},
+  simt_gemm(make_dgrad_a((const float*)dy, g), DgradB{(const float*)w, g},
             DgradEpi<float>{(float*)dx, (const float*)mask, g.c}, g.n * g.h * g.w, g.c, g.k * g.k * g.co, 1, st);
   CE_CHECK_LAUNCH();
   return CE_OK;
@@ -114,7 +114,7 @@ int ce_conv_wgrad(const ce_conv_desc* d, const void* x, const void* dy, float* d
     if (int s = conv_wgrad_tc(g, (const bf16*)x, (const bf16*)dy, part, &splits, sms(), st)) return s;
   } else {
     splits = simt_splits(Mo, 8);
-    simt_gemm(WgradA<float>{(const float*)dy, g.co}, WgradB<float>{FwdA<float>{(const float*)x, g}},
+    simt_gemm(WgradA<float>{(const float*)dy, g.co}, WgradB<float>{make_fwd_a((const float*)x, g)},
               PartialEpi{part, g.co, K}, g.co, K, Mo, splits, st);
   }
   CE_CHECK_LAUNCH();

@@ -30,7 +30,34 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const AF A, const BF B, 
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  // Separable operands (im2col: element offset = row part(m) + column part(k)):
+  // each thread's rows (A) / columns (B) are fixed across the K loop, so their
+  // offset parts are computed once here.
+  size_t a_row[TM];
+  bool a_ok[TM];
+  if constexpr (AF::SEPARABLE) {
+#pragma unroll
+    for (int j = 0; j < TM; ++j) {
+      const int m = m0 + (threadIdx.x >> 4) + 16 * j;
+      a_ok[j] = m < M;
+      a_row[j] = a_ok[j] ? A.row(m) : 0;
+    }
+  }
+  size_t b_col = 0;
+  bool b_ok = false;
+  if constexpr (BF::SEPARABLE) {
+    const int n = n0 + (threadIdx.x & 63);
+    b_ok = n < N;
+    b_col = b_ok ? B.col(n) : 0;
+  }
   for (int k0 = kbeg; k0 < kend; k0 += SG_BK) {
+    if constexpr (AF::SEPARABLE) {  // thread loads column kk = tid % 16 of rows tid/16 + 16 j
+      const int kk = threadIdx.x & 15, k = k0 + kk;
+      const bool kok = k < kend;
+      const size_t ko = kok ? A.col(k) : 0;
+#pragma unroll
+      for (int j = 0; j < TM; ++j) As[kk][(threadIdx.x >> 4) + 16 * j] = (kok && a_ok[j]) ? A.ld(a_row[j] + ko) : 0.f;
+    } else
 #pragma unroll
     for (int e = threadIdx.x; e < BM * SG_BK; e += 256) {
       int mm, kk;
@@ -44,6 +71,14 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const AF A, const BF B, 
       const int m = m0 + mm, k = k0 + kk;
       As[kk][mm] = (m < M && k < kend) ? A(m, k) : 0.f;
     }
+    if constexpr (BF::SEPARABLE) {  // thread loads column nn = tid % 64 of rows tid/64 + 4 j
+      const int nn = threadIdx.x & 63;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int kk = (threadIdx.x >> 6) + 4 * j, k = k0 + kk;
+        Bs[kk][nn] = (b_ok && k < kend) ? B.ld(B.row(k) + b_col) : 0.f;
+      }
+    } else
 #pragma unroll
     for (int e = threadIdx.x; e < SG_BN * SG_BK; e += 256) {
       int nn, kk;
@@ -119,22 +154,35 @@ struct ConvGeom {
 
 // ---------------------------------------------------------------- operand functors
 // forward: A = im2col(x) [m=(n,p,q)][kk=(i,j,c)], B = W [kk][o]
+// im2col of a valid convolution is separable: x offset = row(m) + col(kk) with
+// row = receptive-field origin of output pixel m and col = (tap, channel) offset.
 template <class T>
 struct FwdA {
-  static constexpr bool M_FAST = false;
+  static constexpr bool M_FAST = false, SEPARABLE = true;
   const T* x;
   ConvGeom g;
-  __device__ float operator()(int m, int kk) const {
-    int q = m % g.ow, t = m / g.ow;
-    int p = t % g.oh, n = t / g.oh;
-    int c = kk % g.c, tap = kk / g.c;
-    int j = tap % g.k, i = tap / g.k;
-    size_t off = (((size_t)n * g.h + (p * g.s + i)) * g.w + (q * g.s + j)) * g.c + c;
-    return ldf(x, off);
+  FastDiv d_ow, d_oh, d_c, d_k;
+  __device__ size_t row(int m) const {
+    uint32_t t, q, p, n;
+    d_ow.divmod((uint32_t)m, t, q);
+    d_oh.divmod(t, n, p);
+    return (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
   }
+  __device__ size_t col(int kk) const {
+    uint32_t tap, c, i, j;
+    d_c.divmod((uint32_t)kk, tap, c);
+    d_k.divmod(tap, i, j);
+    return ((size_t)i * g.w + j) * g.c + c;
+  }
+  __device__ float ld(size_t off) const { return ldf(x, off); }
+  __device__ float operator()(int m, int kk) const { return ld(row(m) + col(kk)); }
 };
+template <class T>
+FwdA<T> make_fwd_a(const T* x, const ConvGeom& g) {
+  return FwdA<T>{x, g, FastDiv(g.ow), FastDiv(g.oh), FastDiv(g.c), FastDiv(g.k)};
+}
 struct FwdB {  // W [o][kk] fp32 master
-  static constexpr bool N_FAST = false;
+  static constexpr bool N_FAST = false, SEPARABLE = false;
   const float* w;
   int K;
   __device__ float operator()(int kk, int o) const { return w[(size_t)o * K + kk]; }
@@ -155,15 +203,17 @@ struct FwdEpi {
 // dgrad: A = gather(dY) [m=(n,h,w)][kk=(i,j,o)], B = W^T [kk][c]
 template <class T>
 struct DgradA {
-  static constexpr bool M_FAST = false;
+  static constexpr bool M_FAST = false, SEPARABLE = false;
   const T* dy;
   ConvGeom g;
+  FastDiv d_w, d_h, d_co, d_k;
   __device__ float operator()(int m, int kk) const {
-    int wx = m % g.w, t = m / g.w;
-    int hy = t % g.h, n = t / g.h;
-    int o = kk % g.co, tap = kk / g.co;
-    int j = tap % g.k, i = tap / g.k;
-    int hp = hy - i, wq = wx - j;
+    uint32_t t, wx, hy, n, tap, o, i, j;
+    d_w.divmod((uint32_t)m, t, wx);
+    d_h.divmod(t, n, hy);
+    d_co.divmod((uint32_t)kk, tap, o);
+    d_k.divmod(tap, i, j);
+    int hp = (int)hy - (int)i, wq = (int)wx - (int)j;
     if (hp < 0 || wq < 0) return 0.f;
     if (hp % g.s || wq % g.s) return 0.f;
     hp /= g.s;
@@ -172,8 +222,12 @@ struct DgradA {
     return ldf(dy, (((size_t)n * g.oh + hp) * g.ow + wq) * g.co + o);
   }
 };
+template <class T>
+DgradA<T> make_dgrad_a(const T* dy, const ConvGeom& g) {
+  return DgradA<T>{dy, g, FastDiv(g.w), FastDiv(g.h), FastDiv(g.co), FastDiv(g.k)};
+}
 struct DgradB {  // W[o][i][j][c] read as [kk=(i,j,o)][c]
-  static constexpr bool N_FAST = true;
+  static constexpr bool N_FAST = true, SEPARABLE = false;
   const float* w;
   ConvGeom g;
   __device__ float operator()(int kk, int c) const {
@@ -196,15 +250,18 @@ struct DgradEpi {
 // wgrad: D[o][kk] = sum_m dY[m][o] * im2col(x)[m][kk]; A = dY^T, B = im2col(x)
 template <class T>
 struct WgradA {
-  static constexpr bool M_FAST = true;
+  static constexpr bool M_FAST = true, SEPARABLE = false;
   const T* dy;
   int co;
   __device__ float operator()(int o, int m) const { return ldf(dy, (size_t)m * co + o); }
 };
 template <class T>
-struct WgradB {
-  static constexpr bool N_FAST = true;
+struct WgradB {  // B(k = output pixel m, n = (tap, channel)) = im2col(m, n): separable
+  static constexpr bool N_FAST = true, SEPARABLE = true;
   FwdA<T> im2col;
+  __device__ size_t row(int m) const { return im2col.row(m); }
+  __device__ size_t col(int kk) const { return im2col.col(kk); }
+  __device__ float ld(size_t off) const { return im2col.ld(off); }
   __device__ float operator()(int m, int kk) const { return im2col(m, kk); }
 };
 struct PartialEpi {  // part[split][rows][cols]
@@ -218,40 +275,40 @@ struct PartialEpi {  // part[split][rows][cols]
 // dense forward: y[b][o] = sum_i x[b][i] W[o][i]  (A = x, B = W^T), split-K partials
 template <class T>
 struct DenseXA {
-  static constexpr bool M_FAST = false;
+  static constexpr bool M_FAST = false, SEPARABLE = false;
   const T* x;
   int in;
   __device__ float operator()(int b, int i) const { return ldf(x, (size_t)b * in + i); }
 };
 struct DenseWB {
-  static constexpr bool N_FAST = false;
+  static constexpr bool N_FAST = false, SEPARABLE = false;
   const float* w;
   int in;
   __device__ float operator()(int i, int o) const { return w[(size_t)o * in + i]; }
 };
 // dense dX: dx[b][i] = sum_o g[b][o] W[o][i]
 struct DenseGA {
-  static constexpr bool M_FAST = false;
+  static constexpr bool M_FAST = false, SEPARABLE = false;
   const float* g;
   int out;
   __device__ float operator()(int b, int o) const { return g[(size_t)b * out + o]; }
 };
 struct DenseWN {
-  static constexpr bool N_FAST = true;
+  static constexpr bool N_FAST = true, SEPARABLE = false;
   const float* w;
   int in;
   __device__ float operator()(int o, int i) const { return w[(size_t)o * in + i]; }
 };
 // dense dW: dW[o][i] = sum_b g[b][o] x[b][i]
 struct DenseGT {
-  static constexpr bool M_FAST = true;
+  static constexpr bool M_FAST = true, SEPARABLE = false;
   const float* g;
   int out;
   __device__ float operator()(int o, int b) const { return g[(size_t)b * out + o]; }
 };
 template <class T>
 struct DenseXN {
-  static constexpr bool N_FAST = true;
+  static constexpr bool N_FAST = true, SEPARABLE = false;
   const T* x;
   int in;
   __device__ float operator()(int b, int i) const { return ldf(x, (size_t)b * in + i); }

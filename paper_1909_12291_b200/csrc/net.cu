@@ -228,11 +228,12 @@ void prof_collect(ce_net* net) {
   net->prof_pending.clear();
 }
 
-int pick_splits(long long blocks_per_split, long long K, long long min_chunk, int num_sms) {
-  long long want = (2LL * num_sms + blocks_per_split - 1) / blocks_per_split;
+int pick_splits(long long blocks_per_split, long long K, long long min_chunk, int num_sms, int waves = 2,
+                int max_splits = 64) {
+  long long want = ((long long)waves * num_sms + blocks_per_split - 1) / blocks_per_split;
   long long cap = K / min_chunk;
   if (want > cap) want = cap;
-  if (want > 64) want = 64;
+  if (want > max_splits) want = max_splits;
   if (want < 1) want = 1;
   return (int)want;
 }
@@ -256,7 +257,7 @@ int enqueue_forward(ce_net* net, int n) {
         int s = conv_fwd_tc(g, (const bf16*)in, l.Wbf, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
         if (s != CE_OK) return s;
       } else {
-        simt_gemm(FwdA<T>{(const T*)in, g}, FwdB{l.W, K}, FwdEpi<T>{(T*)l.out, l.b, g.co, l.relu != 0}, M, g.co, K,
+        simt_gemm(make_fwd_a((const T*)in, g), FwdB{l.W, K}, FwdEpi<T>{(T*)l.out, l.b, g.co, l.relu != 0}, M, g.co, K,
                   1, st);
       }
     } else if (l.kind == CE_LAYER_POOL) {
@@ -268,7 +269,7 @@ int enqueue_forward(ce_net* net, int n) {
     } else {
       const int B = n, K = l.in_units, O = l.out_units;
       long long bps = (long long)cdiv(B, SG_BM) * cdiv(O, SG_BN);
-      int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms));
+      int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms, 8, 256));
       Prof pf(net, P_DENSE_FWD, 2.0 * B * K * O, 4.0 * K * O + (in_act ? act_bytes(net) : 4.0) * B * K, 2);
       if (net->use_tc) {
         const bf16* x16 = (const bf16*)in;
@@ -374,7 +375,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
           int s = conv_dgrad_tc(g, (const bf16*)dy, l.Wtbf, (const bf16*)mask, (bf16*)gout, net->num_sms, st);
           if (s != CE_OK) return s;
         } else {
-          simt_gemm(DgradA<T>{dy, g}, DgradB{l.W, g}, DgradEpi<T>{(T*)gout, mask, g.c}, n * g.h * g.w, g.c,
+          simt_gemm(make_dgrad_a(dy, g), DgradB{l.W, g}, DgradEpi<T>{(T*)gout, mask, g.c}, n * g.h * g.w, g.c,
                     g.k * g.k * g.co, 1, st);
         }
         CE_CHECK_LAUNCH();
@@ -389,7 +390,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       } else {
         long long bps = (long long)cdiv(g.co, SG_BM) * cdiv(K, SG_BN);
         splits = simt_splits(Mo, pick_splits(bps, Mo, 512, net->num_sms));
-        simt_gemm(WgradA<T>{dy, g.co}, WgradB<T>{FwdA<T>{(const T*)x, g}}, PartialEpi{net->ws, g.co, K}, g.co, K, Mo,
+        simt_gemm(WgradA<T>{dy, g.co}, WgradB<T>{make_fwd_a((const T*)x, g)}, PartialEpi{net->ws, g.co, K}, g.co, K, Mo,
                   splits, st);
       }
       CE_CHECK_LAUNCH();
@@ -689,7 +690,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         ws = std::max(ws, (size_t)spt * B * l.out_units * 4);
       }
       long long bps = (long long)cdiv(B, SG_BM) * cdiv(l.out_units, SG_BN);
-      int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms));
+      int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms, 8, 256));
       ws = std::max(ws, (size_t)sp * B * l.out_units * 4);
       ws = std::max(ws, (size_t)(kColsumMaxSplits + 64) * l.out_units * 4);
     } else {

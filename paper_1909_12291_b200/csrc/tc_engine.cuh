@@ -56,24 +56,6 @@ struct TcRoles {
 constexpr int TC_TABLE_BYTES = 20480;              // loader lookup tables
 constexpr int TC_MAX_LAG = 8;
 
-// Division by a runtime-invariant divisor d (1 <= d < 2^31) for 0 <= n < 2^31:
-// q = (n * M) >> (32 + l), M = ceil(2^(32+l) / d), l = ceil(log2 d).
-struct FastDiv {
-  uint64_t mul;
-  uint32_t shift, d;
-  FastDiv() = default;
-  __host__ __device__ explicit FastDiv(uint32_t div) : d(div) {
-    uint32_t l = 0;
-    while ((1ull << l) < div) ++l;
-    shift = 32 + l;
-    mul = ((1ull << shift) + div - 1) / div;
-  }
-  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (uint32_t)(((uint64_t)n * mul) >> shift); }
-  __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
-    q = div(n);
-    r = n - q * d;
-  }
-};
 
 // Tile coordinates handed to loaders / epilogues.
 struct TileCoord {
