@@ -113,7 +113,7 @@ def cpu_rate(genomes, splits, budget):
     return len(genomes) / sum(secs) * 3600.0, sum(secs)
 
 
-def run_reference(args, rank):
+def run_reference(args, rank, out_fd):
     """--impl reference: the oracle port of the reference's CPU path, rank 0 only."""
     if rank != 0:
         return 0
@@ -141,7 +141,7 @@ def run_reference(args, rank):
                                        "forward at batch 8 each on the numpy oracle (OpenBLAS, all host threads), "
                                        "extrapolated to each candidate's 2 epochs + val + latency"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line, out_fd)
     return 0
 
 
@@ -195,11 +195,21 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ GPU arm
+def emit(line, out_fd):
+    """Write the single JSON result line to the real stdout (fd saved at start)."""
+    os.write(out_fd, (json.dumps(line) + "\n").encode())
+
+
 def main():
     args = parse_args()
     rank, world, local = dist_env()
+    # Libraries (NCCL's version banner, ptxas, warnings) may print to stdout;
+    # the contract is ONE JSON line there, so route fd 1 to stderr for the run.
+    sys.stdout.flush()
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
     if args.impl == "reference":
-        return run_reference(args, rank)
+        return run_reference(args, rank, out_fd)
     import torch
     from paper_1909_12291_b200 import TrainBudget, native
     from paper_1909_12291_b200.candidate import DATASETS
@@ -318,7 +328,7 @@ def main():
                                           "extrapolated to each candidate's 2 epochs + val + latency; "
                                           f"{time.perf_counter() - t0:.1f} s of CPU work"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line, out_fd)
     if dist is not None:
         dist.destroy_process_group()
     return 0
