@@ -132,10 +132,10 @@ int ce_maxpool_fwd(const ce_conv_desc* d, const void* x, void* y, uint8_t* arg, 
   ConvGeom g = geom(d, false);
   size_t total = (size_t)g.n * g.oh * g.ow * g.c;
   cudaStream_t st = (cudaStream_t)stream;
-  if (d->precision == CE_PREC_BF16)
-    maxpool_fwd_kernel<bf16><<<grid_for(total / 8), 256, 0, st>>>((const bf16*)x, g, (bf16*)y, arg);
-  else
-    maxpool_fwd_kernel<float><<<grid_for(total / 8), 256, 0, st>>>((const float*)x, g, (float*)y, arg);
+  (void)total;
+  int e = d->precision == CE_PREC_BF16 ? launch_maxpool_fwd<bf16>((const bf16*)x, g, (bf16*)y, arg, false, st)
+                                       : launch_maxpool_fwd<float>((const float*)x, g, (float*)y, arg, false, st);
+  if (e) return e;
   CE_CHECK_LAUNCH();
   return CE_OK;
 }
@@ -146,12 +146,11 @@ int ce_maxpool_bwd(const ce_conv_desc* d, const void* dy, const uint8_t* arg, co
   ConvGeom g = geom(d, false);
   size_t total = (size_t)g.n * g.h * g.w * g.c;
   cudaStream_t st = (cudaStream_t)stream;
-  if (d->precision == CE_PREC_BF16)
-    maxpool_bwd_kernel<bf16, bf16><<<grid_for(total / 8), 256, 0, st>>>((const bf16*)dy, arg, g, (const bf16*)mask,
-                                                                     (bf16*)dx);
-  else
-    maxpool_bwd_kernel<float, float><<<grid_for(total / 8), 256, 0, st>>>((const float*)dy, arg, g, (const float*)mask,
-                                                                       (float*)dx);
+  (void)total;
+  int e = d->precision == CE_PREC_BF16
+              ? launch_maxpool_bwd<bf16, bf16>((const bf16*)dy, arg, g, (const bf16*)mask, (bf16*)dx, st)
+              : launch_maxpool_bwd<float, float>((const float*)dy, arg, g, (const float*)mask, (float*)dx, st);
+  if (e) return e;
   CE_CHECK_LAUNCH();
   return CE_OK;
 }

@@ -6,39 +6,64 @@
 // flattens in (c, h, w) order (nn.py:197-199); the permutation is applied to
 // the first dense layer's columns when parameters are loaded.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 
 namespace ce {
 
 // ---------------------------------------------------------------- generic SIMT GEMM
 // D[m, n] = sum_k A(m, k) * B(k, n) over k in the split's range; E(m, n, split, v)
-// consumes each result. 64x64 tile, BK=16, 256 threads, 4x4 outputs per thread.
-constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
+// consumes each result (fp32 check mode). Tile (16*TM) x (16*TN), BK = 16, 256
+// threads as 16 x 16, each thread TM consecutive rows x TN columns (columns
+// tx*4+{0..3} and, for TN = 8, 64+tx*4+{0..3}: conflict-free float4 reads).
+// Shared memory is double-buffered: the next K tile is fetched into registers
+// while the current one is consumed, one barrier per tile.
+constexpr int SG_BM = 64, SG_BN = 128, SG_BK = 16;
 
-template <int TM, class AF, class BF, class EP>
-__global__ void __launch_bounds__(256) simt_gemm_kernel(const AF A, const BF B, const EP E, int M, int N, int K,
+// Epilogues may consume 4 consecutive columns at once: `static constexpr bool
+// VEC4 = true` plus store4(m, n, split, const float* v, count).
+template <class E, class = void>
+struct has_vec4 : std::false_type {};
+template <class E>
+struct has_vec4<E, std::void_t<decltype(E::VEC4)>> : std::bool_constant<E::VEC4> {};
+// ... or in two phases (read-modify-write): Pre prefetch4(m, n, count) for the
+// whole thread tile first, then commit4(m, n, v, count, pre).
+template <class E, class = void>
+struct has_prefetch : std::false_type {};
+template <class E>
+struct has_prefetch<E, std::void_t<typename E::Pre>> : std::true_type {};
+
+inline int simt_tm(int M) { return M <= 32 ? 2 : 4; }
+inline int simt_tn(int N) { return N <= 64 ? 4 : 8; }
+// output tiles per K split, as launched by simt_gemm
+inline long long simt_tiles(int M, int N) {
+  return (long long)cdiv(M, 16 * simt_tm(M)) * cdiv(N, 16 * simt_tn(N));
+}
+
+template <int TM, int TN, class AF, class BF, class EP>
+__global__ void __launch_bounds__(256, 2) simt_gemm_kernel(const AF A, const BF B, const EP E, int M, int N, int K,
                                                        int kchunk) {
-  constexpr int BM = 16 * TM;  // TM rows per thread: 64-row tiles, or 32 for skinny M (batch rows)
-  __shared__ float As[SG_BK][BM + 4];
-  __shared__ float Bs[SG_BK][SG_BN + 4];
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * SG_BN;
+  constexpr int BM = 16 * TM, BN = 16 * TN;
+  constexpr int AL = BM * SG_BK / 256, BL = BN * SG_BK / 256;  // elements per thread per tile
+  __shared__ __align__(16) float As[2][SG_BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][SG_BK][BN + 4];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int kbeg = blockIdx.z * kchunk;
   const int kend = min(K, kbeg + kchunk);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[TM][4];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
   // Separable operands (im2col: element offset = row part(m) + column part(k)):
-  // each thread's rows (A) / columns (B) are fixed across the K loop, so their
-  // offset parts are computed once here.
+  // each thread's rows (A) / column (B) are fixed across the K loop.
   size_t a_row[TM];
   bool a_ok[TM];
   if constexpr (AF::SEPARABLE) {
 #pragma unroll
     for (int j = 0; j < TM; ++j) {
-      const int m = m0 + (threadIdx.x >> 4) + 16 * j;
+      const int m = m0 + ty + 16 * j;
       a_ok[j] = m < M;
       a_row[j] = a_ok[j] ? A.row(m) : 0;
     }
@@ -46,76 +71,138 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const AF A, const BF B, 
   size_t b_col = 0;
   bool b_ok = false;
   if constexpr (BF::SEPARABLE) {
-    const int n = n0 + (threadIdx.x & 63);
+    const int n = n0 + (tid % BN);
     b_ok = n < N;
     b_col = b_ok ? B.col(n) : 0;
   }
-  for (int k0 = kbeg; k0 < kend; k0 += SG_BK) {
-    if constexpr (AF::SEPARABLE) {  // thread loads column kk = tid % 16 of rows tid/16 + 16 j
-      const int kk = threadIdx.x & 15, k = k0 + kk;
+  float ra[AL], rb[BL];
+  auto fetch = [&](int k0) {
+    if constexpr (AF::SEPARABLE) {  // column kk = tid % 16 of rows tid/16 + 16 j
+      const int k = k0 + tx;
       const bool kok = k < kend;
       const size_t ko = kok ? A.col(k) : 0;
 #pragma unroll
-      for (int j = 0; j < TM; ++j) As[kk][(threadIdx.x >> 4) + 16 * j] = (kok && a_ok[j]) ? A.ld(a_row[j] + ko) : 0.f;
-    } else
+      for (int j = 0; j < AL; ++j) ra[j] = (kok && a_ok[j]) ? A.ld(a_row[j] + ko) : 0.f;
+    } else {
 #pragma unroll
-    for (int e = threadIdx.x; e < BM * SG_BK; e += 256) {
-      int mm, kk;
-      if (AF::M_FAST) {
-        mm = e % BM;
-        kk = e / BM;
-      } else {
-        kk = e % SG_BK;
-        mm = e / SG_BK;
+      for (int j = 0; j < AL; ++j) {
+        const int e = tid + 256 * j;
+        const int mm = AF::M_FAST ? e % BM : e / SG_BK, kk = AF::M_FAST ? e / BM : e % SG_BK;
+        const int m = m0 + mm, k = k0 + kk;
+        ra[j] = (m < M && k < kend) ? A(m, k) : 0.f;
       }
-      const int m = m0 + mm, k = k0 + kk;
-      As[kk][mm] = (m < M && k < kend) ? A(m, k) : 0.f;
     }
-    if constexpr (BF::SEPARABLE) {  // thread loads column nn = tid % 64 of rows tid/64 + 4 j
-      const int nn = threadIdx.x & 63;
+    if constexpr (BF::SEPARABLE) {  // column nn = tid % BN of rows tid/BN + (256/BN) j
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int kk = (threadIdx.x >> 6) + 4 * j, k = k0 + kk;
-        Bs[kk][nn] = (b_ok && k < kend) ? B.ld(B.row(k) + b_col) : 0.f;
+      for (int j = 0; j < BL; ++j) {
+        const int k = k0 + tid / BN + (256 / BN) * j;
+        rb[j] = (b_ok && k < kend) ? B.ld(B.row(k) + b_col) : 0.f;
       }
-    } else
+    } else {
 #pragma unroll
-    for (int e = threadIdx.x; e < SG_BN * SG_BK; e += 256) {
-      int nn, kk;
-      if (BF::N_FAST) {
-        nn = e % SG_BN;
-        kk = e / SG_BN;
-      } else {
-        kk = e % SG_BK;
-        nn = e / SG_BK;
+      for (int j = 0; j < BL; ++j) {
+        const int e = tid + 256 * j;
+        const int nn = BF::N_FAST ? e % BN : e / SG_BK, kk = BF::N_FAST ? e / BN : e % SG_BK;
+        const int n = n0 + nn, k = k0 + kk;
+        rb[j] = (n < N && k < kend) ? B(k, n) : 0.f;
       }
-      const int n = n0 + nn, k = k0 + kk;
-      Bs[kk][nn] = (n < N && k < kend) ? B(k, n) : 0.f;
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
+    if constexpr (AF::SEPARABLE) {
+#pragma unroll
+      for (int j = 0; j < AL; ++j) As[buf][tx][ty + 16 * j] = ra[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < AL; ++j) {
+        const int e = tid + 256 * j;
+        const int mm = AF::M_FAST ? e % BM : e / SG_BK, kk = AF::M_FAST ? e / BM : e % SG_BK;
+        As[buf][kk][mm] = ra[j];
+      }
+    }
+    if constexpr (BF::SEPARABLE) {
+#pragma unroll
+      for (int j = 0; j < BL; ++j) Bs[buf][tid / BN + (256 / BN) * j][tid % BN] = rb[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < BL; ++j) {
+        const int e = tid + 256 * j;
+        const int nn = BF::N_FAST ? e % BN : e / SG_BK, kk = BF::N_FAST ? e / BN : e % SG_BK;
+        Bs[buf][kk][nn] = rb[j];
+      }
+    }
+  };
+  if (kbeg < kend) {
+    fetch(kbeg);
+    stash(0);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = kbeg; k0 < kend; k0 += SG_BK) {
+    const bool more = k0 + SG_BK < kend;
+    if (more) fetch(k0 + SG_BK);
 #pragma unroll
     for (int kk = 0; kk < SG_BK; ++kk) {
-      float a[TM], b[4];
+      float a[TM], b[TN];
+      if constexpr (TM == 4) {
+        const float4 v = *(const float4*)&As[buf][kk][ty * 4];
+        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+      } else {
+        const float2 v = *(const float2*)&As[buf][kk][ty * 2];
+        a[0] = v.x; a[1] = v.y;
+      }
 #pragma unroll
-      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      for (int h = 0; h < TN / 4; ++h) {
+        const float4 v = *(const float4*)&Bs[buf][kk][64 * h + tx * 4];
+        b[4 * h] = v.x; b[4 * h + 1] = v.y; b[4 * h + 2] = v.z; b[4 * h + 3] = v.w;
+      }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
+    if (more) stash(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int m = m0 + ty * TM + i;
     if (m >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int n = n0 + tx * 4 + j;
-      if (n < N) E(m, n, blockIdx.z, acc[i][j]);
+    for (int h = 0; h < TN / 4; ++h) {
+      const int n = n0 + 64 * h + tx * 4;
+      if (n >= N) continue;
+      if constexpr (has_prefetch<EP>::value) {
+        continue;  // handled below: all loads first, then all updates
+      } else if constexpr (has_vec4<EP>::value) {
+        E.store4(m, n, blockIdx.z, &acc[i][4 * h], min(4, N - n));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (n + j < N) E(m, n + j, blockIdx.z, acc[i][4 * h + j]);
+      }
     }
+  }
+  if constexpr (has_prefetch<EP>::value) {
+    // read-modify-write epilogues: issue every load of the thread's tile before
+    // the first store (stores through the same pointers would otherwise pin
+    // each group's loads behind the previous group's stores)
+    typename EP::Pre pre[TM][TN / 4];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int h = 0; h < TN / 4; ++h) {
+        const int m = m0 + ty * TM + i, n = n0 + 64 * h + tx * 4;
+        if (m < M && n < N) pre[i][h] = E.prefetch4(m, n, min(4, N - n));
+      }
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int h = 0; h < TN / 4; ++h) {
+        const int m = m0 + ty * TM + i, n = n0 + 64 * h + tx * 4;
+        if (m < M && n < N) E.commit4(m, n, &acc[i][4 * h], min(4, N - n), pre[i][h]);
+      }
   }
 }
 
@@ -126,13 +213,16 @@ inline void simt_gemm(const AF& A, const BF& B, const EP& E, int M, int N, int K
   kchunk = cdiv(kchunk, SG_BK) * SG_BK;
   splits = cdiv(K, kchunk);
   if (splits < 1) splits = 1;
-  if (M <= 32) {
-    dim3 grid(cdiv(M, 32), cdiv(N, SG_BN), splits);
-    simt_gemm_kernel<2><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
-  } else {
-    dim3 grid(cdiv(M, SG_BM), cdiv(N, SG_BN), splits);
-    simt_gemm_kernel<4><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
-  }
+  const int tm = simt_tm(M), tn = simt_tn(N);
+  dim3 grid(cdiv(M, 16 * tm), cdiv(N, 16 * tn), splits);
+  if (tm == 2 && tn == 4)
+    simt_gemm_kernel<2, 4><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
+  else if (tm == 2)
+    simt_gemm_kernel<2, 8><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
+  else if (tn == 4)
+    simt_gemm_kernel<4, 4><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
+  else
+    simt_gemm_kernel<4, 8><<<grid, 256, 0, st>>>(A, B, E, M, N, K, kchunk);
 }
 
 // Number of K splits used by simt_gemm for a requested split count.
@@ -267,8 +357,17 @@ struct WgradB {  // B(k = output pixel m, n = (tap, channel)) = im2col(m, n): se
 struct PartialEpi {  // part[split][rows][cols]
   float* part;
   int rows, cols;
+  static constexpr bool VEC4 = true;
   __device__ void operator()(int r, int c, int split, float v) const {
     part[((size_t)split * rows + r) * cols + c] = v;
+  }
+  __device__ void store4(int r, int c, int split, const float* v, int cnt) const {
+    const size_t off = ((size_t)split * rows + r) * cols + c;
+    if (cnt == 4 && (off & 3) == 0) {
+      *(float4*)(part + off) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+      for (int j = 0; j < cnt; ++j) part[off + j] = v[j];
+    }
   }
 };
 
@@ -354,6 +453,39 @@ struct DenseSgdEpi {
     w[off] = wv;
     vel[off] = vv;
     if (wbf) wbf[off] = __float2bfloat16_rn(wv);
+  }
+  struct Pre {
+    float4 w, v;
+  };
+  __device__ Pre prefetch4(int o, int i, int cnt) const {
+    const size_t off = (size_t)o * in + i;
+    Pre p;
+    if (cnt == 4 && (off & 3) == 0) {
+      p.w = *(const float4*)(w + off);
+      p.v = *(const float4*)(vel + off);
+    }
+    return p;
+  }
+  __device__ void commit4(int o, int i, const float* g, int cnt, Pre p) const {
+    const size_t off = (size_t)o * in + i;
+    if (cnt == 4 && (off & 3) == 0) {
+      if (gw) *(float4*)(gw + off) = make_float4(g[0], g[1], g[2], g[3]);
+      sgd_update(p.w.x, p.v.x, g[0], lr, mu);
+      sgd_update(p.w.y, p.v.y, g[1], lr, mu);
+      sgd_update(p.w.z, p.v.z, g[2], lr, mu);
+      sgd_update(p.w.w, p.v.w, g[3], lr, mu);
+      *(float4*)(w + off) = p.w;
+      *(float4*)(vel + off) = p.v;
+      if (wbf) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(p.w.x, p.w.y), hi = __floats2bfloat162_rn(p.w.z, p.w.w);
+        uint2 u;
+        u.x = *(const uint32_t*)&lo;
+        u.y = *(const uint32_t*)&hi;
+        *(uint2*)(wbf + off) = u;
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) (*this)(o, i + j, 0, g[j]);
+    }
   }
 };
 

@@ -265,11 +265,13 @@ int enqueue_forward(ce_net* net, int n) {
       g.n = n;
       size_t total = (size_t)n * g.oh * g.ow * g.c;
       Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)n * g.h * g.w * g.c + total) + total);
-      maxpool_fwd_kernel<T><<<grid_for(total / 8), 256, 0, st>>>((const T*)in, g, (T*)l.out, l.arg);
+      if (int e = launch_maxpool_fwd<T>((const T*)in, g, (T*)l.out, l.arg, l.mask_in, st)) return e;
+      CE_CHECK_LAUNCH();
     } else {
       const int B = n, K = l.in_units, O = l.out_units;
-      long long bps = (long long)cdiv(B, SG_BM) * cdiv(O, SG_BN);
+      long long bps = simt_tiles(B, O);
       int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms, 8, 256));
+      while (splits > 1 && (size_t)splits * B * O * 4 > net->ws_bytes) splits = simt_splits(K, splits - 1);
       Prof pf(net, P_DENSE_FWD, 2.0 * B * K * O, 4.0 * K * O + (in_act ? act_bytes(net) : 4.0) * B * K, 2);
       if (net->use_tc) {
         const bf16* x16 = (const bf16*)in;
@@ -388,8 +390,9 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         if (s != CE_OK) return s;
         pf.bytes += 4.0 * splits * g.co * K;
       } else {
-        long long bps = (long long)cdiv(g.co, SG_BM) * cdiv(K, SG_BN);
+        long long bps = simt_tiles(g.co, K);
         splits = simt_splits(Mo, pick_splits(bps, Mo, 512, net->num_sms));
+        while (splits > 1 && (size_t)splits * g.co * K * 4 > net->ws_bytes) splits = simt_splits(Mo, splits - 1);
         simt_gemm(WgradA<T>{dy, g.co}, WgradB<T>{make_fwd_a((const T*)x, g)}, PartialEpi{net->ws, g.co, K}, g.co, K, Mo,
                   splits, st);
       }
@@ -407,8 +410,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         ConvGeom g = l.g;
         g.n = n;
         size_t total = (size_t)n * g.h * g.w * g.c;
-        Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)n * g.oh * g.ow * g.c * 2 + total));
-        maxpool_bwd_kernel<T, T><<<grid_for(total / 8), 256, 0, st>>>((const T*)gin, l.arg, g, mask, (T*)gout);
+        // algorithmic bytes: dy + dx in the activation type, argmax 1 B per pooled element; the ReLU
+        // mask of the input is folded into the argmax by the forward (kPoolDead)
+        Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)n * g.oh * g.ow * g.c + total) +
+                                      (double)n * g.oh * g.ow * g.c);
+        if (int e = launch_maxpool_bwd<T, T>((const T*)gin, l.arg, g, (const T*)nullptr, (T*)gout, st)) return e;
         CE_CHECK_LAUNCH();
       }
     }
@@ -689,7 +695,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         int spt = dense_fwd_splits(l.out_units, l.in_units, net->num_sms);
         ws = std::max(ws, (size_t)spt * B * l.out_units * 4);
       }
-      long long bps = (long long)cdiv(B, SG_BM) * cdiv(l.out_units, SG_BN);
+      long long bps = simt_tiles((int)B, l.out_units);
       int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms, 8, 256));
       ws = std::max(ws, (size_t)sp * B * l.out_units * 4);
       ws = std::max(ws, (size_t)(kColsumMaxSplits + 64) * l.out_units * 4);
@@ -702,7 +708,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         l.wn = (size_t)l.g.co * K;
         l.bn = l.g.co;
         long long Mo = (long long)B * l.g.oh * l.g.ow;
-        long long bps = (long long)cdiv(l.g.co, SG_BM) * cdiv(K, SG_BN);
+        long long bps = simt_tiles(l.g.co, K);
         int sp = simt_splits((int)Mo, pick_splits(bps, Mo, 512, net->num_sms));
         sp = std::max(sp, conv_wgrad_tc_max_splits(l.g, (int)B, net->num_sms));
         ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);

@@ -73,8 +73,17 @@ __device__ __forceinline__ void load8(const T* p, float (&v)[8]);
 template <class T>
 __device__ __forceinline__ void store8(T* p, const float (&v)[8]);
 
-template <class T>
-__global__ void maxpool_fwd_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y, uint8_t* __restrict__ arg) {
+// Window size K and stride S are template parameters (search space: K in {2,3},
+// S in {1,2,3}) so every tap load is issued before the first compare.
+// relu_flag: the pool input is a ReLU output, so the gradient of a window
+// whose max is not > 0 is zero (mask(x > 0) at the argmax position); the
+// forward stores argmax 0xFF for such windows, which never matches a tap in
+// the backward, and the mask tensor is not read there at all.
+constexpr uint8_t kPoolDead = 0xFF;
+
+template <class T, int K, int S>
+__global__ void __launch_bounds__(256) maxpool_fwd_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y,
+                                                          uint8_t* __restrict__ arg, bool relu_flag) {
   const int cg = g.c / 8;
   const int total = g.n * g.oh * g.ow * cg;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -83,22 +92,26 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ x, ConvGeom g, T* __res
     const int q = t % g.ow;
     t /= g.ow;
     const int p = t % g.oh, n = t / g.oh;
-    const T* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c + c0;
-    float best[8];
-    uint8_t bi[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    load8(base, best);
-    for (int i = 0; i < g.k; ++i)
-      for (int j = 0; j < g.k; ++j) {
-        float v[8];
-        load8(base + ((size_t)i * g.w + j) * g.c, v);
-        const uint8_t idx = (uint8_t)(i * g.k + j);
+    const T* base = x + (((size_t)n * g.h + p * S) * g.w + q * S) * g.c + c0;
+    float v[K * K][8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (v[u] > best[u]) {
-            best[u] = v[u];
-            bi[u] = idx;
-          }
-      }
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) load8(base + ((size_t)i * g.w + j) * g.c, v[i * K + j]);
+    float best[8];
+    uint8_t bi[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      best[u] = v[0][u];
+      bi[u] = 0;
+#pragma unroll
+      for (int tap = 1; tap < K * K; ++tap)
+        if (v[tap][u] > best[u]) {
+          best[u] = v[tap][u];
+          bi[u] = (uint8_t)tap;
+        }
+      if (relu_flag && !(best[u] > 0.f)) bi[u] = kPoolDead;
+    }
     const size_t o = (size_t)e * 8;
     store8(y + o, best);
     if (arg) *(uint2*)(arg + o) = *(const uint2*)bi;
@@ -106,10 +119,12 @@ __global__ void maxpool_fwd_kernel(const T* __restrict__ x, ConvGeom g, T* __res
 }
 
 // gather form: dx[n,h,w,c] = sum over windows (p,q) whose argmax hits (h,w),
-// accumulated in window order; optional ReLU mask of the pool input.
-template <class T, class TG>
-__global__ void maxpool_bwd_kernel(const TG* __restrict__ dy, const uint8_t* __restrict__ arg, ConvGeom g,
-                                   const T* __restrict__ mask, TG* __restrict__ dx) {
+// accumulated in window order; optional ReLU mask of the pool input (the
+// kernel-level ABI; the network path folds the mask into the argmax).
+template <class T, class TG, int K, int S>
+__global__ void __launch_bounds__(256) maxpool_bwd_kernel(const TG* __restrict__ dy, const uint8_t* __restrict__ arg,
+                                                          ConvGeom g, const T* __restrict__ mask, TG* __restrict__ dx) {
+  constexpr int W = (K + S - 1) / S;  // windows covering a pixel along one axis
   const int cg = g.c / 8;
   const int total = g.n * g.h * g.w * cg;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -118,22 +133,35 @@ __global__ void maxpool_bwd_kernel(const TG* __restrict__ dy, const uint8_t* __r
     const int wx = t % g.w;
     t /= g.w;
     const int hy = t % g.h, n = t / g.h;
+    // highest window index covering hy / wx, then walk down W candidates
+    const int p_top = min(hy / S, g.oh - 1), q_top = min(wx / S, g.ow - 1);
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const int p_lo = hy - g.k + 1 > 0 ? (hy - g.k + 1 + g.s - 1) / g.s : 0;
-    const int p_hi = min(hy / g.s, g.oh - 1);
-    const int q_lo = wx - g.k + 1 > 0 ? (wx - g.k + 1 + g.s - 1) / g.s : 0;
-    const int q_hi = min(wx / g.s, g.ow - 1);
-    for (int p = p_lo; p <= p_hi; ++p)
-      for (int q = q_lo; q <= q_hi; ++q) {
-        const size_t o = (((size_t)n * g.oh + p) * g.ow + q) * g.c + c0;
-        const uint8_t hit = (uint8_t)((hy - p * g.s) * g.k + (wx - q * g.s));
-        uint2 a2 = *(const uint2*)(arg + o);
-        const uint8_t* a = (const uint8_t*)&a2;
-        float v[8];
-        load8(dy + o, v);
+    uint2 a2[W][W];
+    float v[W][W][8];
+    bool ok[W][W];
+#pragma unroll
+    for (int di = 0; di < W; ++di)
+#pragma unroll
+      for (int dj = 0; dj < W; ++dj) {
+        const int p = p_top - (W - 1 - di), q = q_top - (W - 1 - dj);
+        ok[di][dj] = p >= 0 && q >= 0 && hy - p * S < K && wx - q * S < K;
+        if (ok[di][dj]) {
+          const size_t o = (((size_t)n * g.oh + p) * g.ow + q) * g.c + c0;
+          a2[di][dj] = *(const uint2*)(arg + o);
+          load8(dy + o, v[di][dj]);
+        }
+      }
+#pragma unroll
+    for (int di = 0; di < W; ++di)
+#pragma unroll
+      for (int dj = 0; dj < W; ++dj) {
+        if (!ok[di][dj]) continue;
+        const int p = p_top - (W - 1 - di), q = q_top - (W - 1 - dj);
+        const uint8_t hit = (uint8_t)((hy - p * S) * K + (wx - q * S));
+        const uint8_t* a = (const uint8_t*)&a2[di][dj];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (a[u] == hit) acc[u] += v[u];
+          if (a[u] == hit) acc[u] += v[di][dj][u];
       }
     const size_t off = (size_t)e * 8;
     if (mask) {
@@ -145,6 +173,26 @@ __global__ void maxpool_bwd_kernel(const TG* __restrict__ dy, const uint8_t* __r
     }
     store8(dx + off, acc);
   }
+}
+
+template <class T>
+int launch_maxpool_fwd(const T* x, const ConvGeom& g, T* y, uint8_t* arg, bool relu_flag, cudaStream_t st) {
+  const int grid = grid_for((size_t)g.n * g.oh * g.ow * (g.c / 8));
+#define CE_POOL_F(KK, SS) \
+  if (g.k == KK && g.s == SS) { maxpool_fwd_kernel<T, KK, SS><<<grid, 256, 0, st>>>(x, g, y, arg, relu_flag); return CE_OK; }
+  CE_POOL_F(2, 1) CE_POOL_F(2, 2) CE_POOL_F(2, 3) CE_POOL_F(3, 1) CE_POOL_F(3, 2) CE_POOL_F(3, 3)
+#undef CE_POOL_F
+  return fail(CE_EINVAL, "max pool size %d stride %d not supported (size 2..3, stride 1..3)", g.k, g.s);
+}
+
+template <class T, class TG>
+int launch_maxpool_bwd(const TG* dy, const uint8_t* arg, const ConvGeom& g, const T* mask, TG* dx, cudaStream_t st) {
+  const int grid = grid_for((size_t)g.n * g.h * g.w * (g.c / 8));
+#define CE_POOL_B(KK, SS) \
+  if (g.k == KK && g.s == SS) { maxpool_bwd_kernel<T, TG, KK, SS><<<grid, 256, 0, st>>>(dy, arg, g, mask, dx); return CE_OK; }
+  CE_POOL_B(2, 1) CE_POOL_B(2, 2) CE_POOL_B(2, 3) CE_POOL_B(3, 1) CE_POOL_B(3, 2) CE_POOL_B(3, 3)
+#undef CE_POOL_B
+  return fail(CE_EINVAL, "max pool size %d stride %d not supported (size 2..3, stride 1..3)", g.k, g.s);
 }
 
 // ---------------------------------------------------------------- reductions
