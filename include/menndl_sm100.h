@@ -153,6 +153,67 @@ int ce_maxpool_fwd(const ce_conv_desc* d, const void* x, void* y, uint8_t* arg, 
 int ce_maxpool_bwd(const ce_conv_desc* d, const void* dy, const uint8_t* arg, const void* mask, void* dx,
                    void* stream);
 
+/* Batch gather + normalise (data.py:65-66 as_float, evaluator.py:166 x[idx]):
+ * out[b] = pixels[idx[b]] / 255 for b < n. pixels: device u8 NCHW (count, c, h, w);
+ * idx: device int32; out: NHWC with channels zero-padded to c_store (>= c),
+ * bf16 or float32 by `precision`.                                               */
+int ce_gather_u8_normalize(const uint8_t* pixels, int c, int h, int w, const int32_t* idx, int n, int c_store,
+                           int precision, void* out, void* stream);
+
+/* Dense layer passes (replaces Dense.forward / Dense.backward, nn.py:225-240).
+ * fp32: x [n][in] float32, w [out][in] float32 master (the FFMA path).
+ * bf16: x [n][in_pad] bf16 and w16 [out][in_pad] bf16 mirror of w, in_pad = in
+ *       rounded up to 8 with zero columns (tensor-core path); w is still the
+ *       float32 master (read by the fused SGD).
+ * y / dy / dw / db are float32. dx and mask have the activation type (bf16 in
+ * bf16 mode, laid out [n][in] -- no padding -- ; float32 otherwise).          */
+typedef struct ce_dense_desc {
+  int n;          /* batch rows (bf16: <= 256)                                 */
+  int in, out;    /* units                                                    */
+  int precision;  /* CE_PREC_*                                                */
+} ce_dense_desc;
+
+/* Momentum SGD fused into a gradient pass (sgd_step, nn.py:306-322):
+ * v <- momentum*v - lr*g ; w <- w + v, in fp32 without contraction.          */
+typedef struct ce_sgd_args {
+  float lr, momentum;
+  float* vel_w;  /* velocity of w (same layout as w), updated in place          */
+  float* vel_b;  /* velocity of b                                               */
+} ce_sgd_args;
+
+size_t ce_dense_workspace_bytes(const ce_dense_desc* d);
+/* y = x @ w^T + b                                                              */
+int ce_dense_fwd(const ce_dense_desc* d, const void* x, const float* w, const void* w16, const float* b, float* y,
+                 void* workspace, size_t ws_bytes, void* stream);
+/* dx = dy @ w (pre-update weights; optional, skipped when dx is NULL), gated by
+ * (mask > 0) when mask is given; dw = dy^T x and db = sum_n dy (each optional).
+ * With sgd != NULL, w / b (and w16 in bf16 mode) are updated in place after dx. */
+int ce_dense_bwd(const ce_dense_desc* d, const void* x, const float* dy, float* w, void* w16, float* b, void* dx,
+                 const void* mask, float* dw, float* db, const ce_sgd_args* sgd, void* workspace, size_t ws_bytes,
+                 void* stream);
+
+/* softmax_cross_entropy (nn.py:287-303) on device float32 logits [n][k], int64
+ * labels: *loss (device float) = -mean(logp[label]), grad = (softmax - onehot)/n.
+ * n <= 1024. Labels outside [0, k) make the loss NaN (the host mirror raises
+ * ValueError before calling, as the reference does).                           */
+int ce_softmax_xent(const float* logits, const int64_t* labels, int n, int k, float* loss, float* grad, void* stream);
+
+/* sgd_step on one parameter tensor (nn.py:306-322), bit-exact fp32:
+ * vel <- momentum*vel - lr*g ; w <- w + vel. lr > 0 and 0 <= momentum < 1
+ * (nn.py:308-311) else CE_EINVAL.                                              */
+int ce_sgd_momentum(float* w, float* vel, const float* g, size_t count, float lr, float momentum, void* stream);
+
+/* numpy Generator(PCG64(state, inc)) advanced by `skip` draws, then
+ * .uniform(low, high, size=count).astype(float32) (nn.py:44-46), bit-exact.    */
+int ce_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t skip,
+                     double low, double high, float* out, size_t count, void* stream);
+
+/* Dense columns between the reference flatten order (c, h, w) (nn.py:186-202)
+ * and the device NHWC order (h, w, c_store), padded channels zero.
+ * direction 0: src [rows][c*hw] -> dst [rows][hw*c_store]; 1: the inverse.     */
+int ce_permute_flatten_weights(const float* src, size_t rows, int c, int c_store, int hw, int direction, float* dst,
+                               void* stream);
+
 /* ---- instrumentation (bench.py) ------------------------------------------- */
 /* kernels this process has launched through the library (graph replays count every node) */
 long long ce_launch_count(void);

@@ -153,6 +153,12 @@ struct DenseDwSgdEpi {
     const int i = c.m0 + row;
     if (i >= in || o0 >= out) return;
     const int n = out - o0 < 16 ? out - o0 : 16;
+    if (!w) {  // gradient only (kernel-level ce_dense_bwd without SGD)
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (u < n) gw[(size_t)(o0 + u) * in + i] = v[u];
+      return;
+    }
     float wv[16], vv[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -170,7 +176,7 @@ struct DenseDwSgdEpi {
         sgd_update(wv[u], vv[u], v[u], lr, mu);
         __stcs(w + off, wv[u]);
         __stcs(vel + off, vv[u]);
-        wb[(size_t)(o0 + u) * in_pad + i] = __float2bfloat16_rn(wv[u]);
+        if (wb) wb[(size_t)(o0 + u) * in_pad + i] = __float2bfloat16_rn(wv[u]);
       }
     }
   }

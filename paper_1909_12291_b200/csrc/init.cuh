@@ -72,15 +72,18 @@ __device__ __forceinline__ size_t init_dev_index(const InitLayout& L, size_t r) 
 
 constexpr int kInitChunk = 2048;
 
+// numpy Generator.uniform(lo, lo + range): lo + range * next_double, in double,
+// then cast to float32 (the .astype of nn.py:46). Draw r of the stream (after
+// `skip`) lands at init_dev_index(L, r). Kaiming: lo = -limit, range = 2*limit.
 __global__ void kaiming_uniform_kernel(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo,
-                                       size_t count, double limit, InitLayout L, float* __restrict__ w) {
+                                       unsigned long long skip, size_t count, double lo, double range, InitLayout L,
+                                       float* __restrict__ w) {
   const u128 state = ((u128)st_hi << 64) | st_lo;
   const u128 inc = ((u128)inc_hi << 64) | inc_lo;
   const size_t nchunks = (count + kInitChunk - 1) / kInitChunk;
-  const double lo = -limit, range = 2.0 * limit;
   for (size_t ch = blockIdx.x * (size_t)blockDim.x + threadIdx.x; ch < nchunks;
        ch += (size_t)gridDim.x * blockDim.x) {
-    u128 s = pcg_advance(state, inc, (unsigned long long)(ch * kInitChunk));
+    u128 s = pcg_advance(state, inc, skip + (unsigned long long)(ch * kInitChunk));
     const size_t r1 = count < (ch + 1) * kInitChunk ? count : (ch + 1) * kInitChunk;
     for (size_t r = ch * kInitChunk; r < r1; ++r) {
       const uint64_t x = pcg_next(s, inc);

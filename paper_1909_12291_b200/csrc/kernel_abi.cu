@@ -4,6 +4,8 @@
 // runtime (net.cu) calls the same kernels directly.
 #include "ops.cuh"
 #include "conv_tc.cuh"
+#include "dense_tc.cuh"
+#include "init.cuh"
 
 using namespace ce;
 
@@ -41,6 +43,34 @@ int sms() {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n;
 }
+
+__global__ void sgd_momentum_kernel(float* __restrict__ w, float* __restrict__ vel, const float* __restrict__ g,
+                                    size_t count, float lr, float mu) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+    float wv = w[e], vv = vel[e];
+    sgd_update(wv, vv, g[e], lr, mu);
+    w[e] = wv;
+    vel[e] = vv;
+  }
+}
+
+int check_dense(const ce_dense_desc* d) {
+  if (!d) return fail(CE_EINVAL, "null descriptor");
+  if (d->n < 1 || d->in < 1 || d->out < 1) return fail(CE_EINVAL, "bad dense descriptor (n=%d in=%d out=%d)", d->n, d->in, d->out);
+  if (d->precision != CE_PREC_BF16 && d->precision != CE_PREC_FP32) return fail(CE_EINVAL, "bad precision");
+  if (d->precision == CE_PREC_BF16 && d->n > 256) return fail(CE_EINVAL, "bf16 dense supports n <= 256 (got %d)", d->n);
+  return CE_OK;
+}
+
+int pad8(int v) { return (v + 7) / 8 * 8; }
+
+// split-K partial count of the dense forward for this descriptor
+int dense_fwd_part_splits(const ce_dense_desc* d) {
+  if (d->precision == CE_PREC_BF16) return dense_fwd_splits(d->out, d->in, sms());
+  return simt_splits(d->in, pick_splits(simt_tiles(d->n, d->out), d->in, 256, sms(), 8, 256));
+}
+
+size_t align256(size_t v) { return (v + 255) / 256 * 256; }
 
 size_t wgrad_ws(const ConvGeom& g, bool tc) {
   const int K = g.k * g.k * g.c, Mo = g.n * g.oh * g.ow;
@@ -151,6 +181,159 @@ int ce_maxpool_bwd(const ce_conv_desc* d, const void* dy, const uint8_t* arg, co
               ? launch_maxpool_bwd<bf16, bf16>((const bf16*)dy, arg, g, (const bf16*)mask, (bf16*)dx, st)
               : launch_maxpool_bwd<float, float>((const float*)dy, arg, g, (const float*)mask, (float*)dx, st);
   if (e) return e;
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+
+int ce_gather_u8_normalize(const uint8_t* pixels, int c, int h, int w, const int32_t* idx, int n, int c_store,
+                           int precision, void* out, void* stream) {
+  if (!pixels || !idx || !out || n < 1 || c < 1 || h < 1 || w < 1 || c_store < c)
+    return fail(CE_EINVAL, "bad gather arguments (n=%d c=%d c_store=%d)", n, c, c_store);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int HW = h * w;
+  dim3 grid(cdiv(HW, 256), n);
+  if (precision == CE_PREC_BF16)
+    gather_u8_kernel<bf16><<<grid, 256, 0, st>>>(pixels, nullptr, idx, nullptr, 0, 0, 0, n, c, c_store, HW, (bf16*)out,
+                                                 nullptr);
+  else if (precision == CE_PREC_FP32)
+    gather_u8_kernel<float><<<grid, 256, 0, st>>>(pixels, nullptr, idx, nullptr, 0, 0, 0, n, c, c_store, HW,
+                                                  (float*)out, nullptr);
+  else
+    return fail(CE_EINVAL, "bad precision");
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+size_t ce_dense_workspace_bytes(const ce_dense_desc* d) {
+  if (check_dense(d)) return 0;
+  const size_t fwd = (size_t)dense_fwd_part_splits(d) * d->n * d->out * 4;
+  const size_t gbf = d->precision == CE_PREC_BF16 ? align256((size_t)d->n * pad8(d->out) * 2) : 0;
+  const size_t bwd = gbf + (size_t)(kColsumMaxSplits + 64) * d->out * 4;
+  return (fwd > bwd ? fwd : bwd) + 256;
+}
+
+int ce_dense_fwd(const ce_dense_desc* d, const void* x, const float* w, const void* w16, const float* b, float* y,
+                 void* workspace, size_t ws_bytes, void* stream) {
+  if (int s = check_dense(d)) return s;
+  if (!x || !y) return fail(CE_EINVAL, "null dense operand");
+  if (!workspace || ws_bytes < ce_dense_workspace_bytes(d)) return fail(CE_EINVAL, "dense workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* part = (float*)workspace;
+  int splits;
+  if (d->precision == CE_PREC_BF16) {
+    if (!w16) return fail(CE_EINVAL, "bf16 dense needs the bf16 weight mirror");
+    const int in_pad = pad8(d->in);
+    if (int s = dense_fwd_tc((const bf16*)x, in_pad, (const bf16*)w16, d->in, in_pad, d->out, d->n, part, &splits,
+                             sms(), st))
+      return s;
+  } else {
+    if (!w) return fail(CE_EINVAL, "null dense weights");
+    splits = dense_fwd_part_splits(d);
+    simt_gemm(DenseXA<float>{(const float*)x, d->in}, DenseWB{w, d->in}, PartialEpi{part, d->n, d->out}, d->n, d->out,
+              d->in, splits, st);
+  }
+  CE_CHECK_LAUNCH();
+  launch_dense_reduce(part, splits, d->n, d->out, b, y, st);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+int ce_dense_bwd(const ce_dense_desc* d, const void* x, const float* dy, float* w, void* w16, float* b, void* dx,
+                 const void* mask, float* dw, float* db, const ce_sgd_args* sgd, void* workspace, size_t ws_bytes,
+                 void* stream) {
+  if (int s = check_dense(d)) return s;
+  if (!x || !dy) return fail(CE_EINVAL, "null dense operand");
+  if (!workspace || ws_bytes < ce_dense_workspace_bytes(d)) return fail(CE_EINVAL, "dense workspace too small");
+  if (sgd) {
+    if (!(sgd->lr > 0.f)) return fail(CE_EINVAL, "lr must be positive, got %g", (double)sgd->lr);
+    if (!(sgd->momentum >= 0.f && sgd->momentum < 1.f))
+      return fail(CE_EINVAL, "momentum must lie in [0, 1), got %g", (double)sgd->momentum);
+    if (!w || !b || !sgd->vel_w || !sgd->vel_b) return fail(CE_EINVAL, "fused SGD needs w, b and both velocities");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = d->n, in = d->in, out = d->out;
+  const float lr = sgd ? sgd->lr : 0.f, mu = sgd ? sgd->momentum : 0.f;
+  float* bpart;
+  if (d->precision == CE_PREC_BF16) {
+    if (!w16) return fail(CE_EINVAL, "bf16 dense needs the bf16 weight mirror");
+    const int in_pad = pad8(in), out_pad = pad8(out);
+    bf16* gbf = (bf16*)workspace;
+    bpart = (float*)((char*)workspace + align256((size_t)n * out_pad * 2));
+    f32_to_bf16_pad_kernel<<<grid_for((size_t)n * out_pad), 256, 0, st>>>(dy, n, out, out_pad, gbf);
+    CE_CHECK_LAUNCH();
+    if (dx) {
+      if (int s = dense_dx_tc((const bf16*)w16, gbf, in, in_pad, out, out_pad, n, (const bf16*)mask, (bf16*)dx, sms(),
+                              st))
+        return s;
+    }
+    if (sgd || dw) {
+      if (int s = dense_dw_sgd_tc((const bf16*)x, in_pad, gbf, in, in_pad, out, out_pad, n, sgd ? w : nullptr,
+                                  sgd ? sgd->vel_w : nullptr, dw, sgd ? (bf16*)w16 : nullptr, lr, mu, sms(), st))
+        return s;
+    }
+  } else {
+    if (!w && dx) return fail(CE_EINVAL, "null dense weights");
+    bpart = (float*)workspace;
+    if (dx)
+      simt_gemm(DenseGA{dy, out}, DenseWN{w, in}, DenseDxEpi<float, float>{(float*)dx, (const float*)mask, in}, n, in,
+                out, 1, st);
+    if (sgd || dw) {
+      DenseSgdEpi se{sgd ? w : nullptr, sgd ? sgd->vel_w : nullptr, dw, nullptr, in, lr, mu};
+      simt_gemm(DenseGT{dy, out}, DenseXN<float>{(const float*)x, in}, se, out, in, n, 1, st);
+    }
+  }
+  CE_CHECK_LAUNCH();
+  if (sgd || db) {
+    const int bs = colsum(dy, n, out, bpart, st);
+    launch_bias_sgd(bpart, bs, out, sgd ? b : nullptr, sgd ? sgd->vel_b : nullptr, db, lr, mu, st);
+    CE_CHECK_LAUNCH();
+  }
+  return CE_OK;
+}
+
+int ce_softmax_xent(const float* logits, const int64_t* labels, int n, int k, float* loss, float* grad,
+                    void* stream) {
+  if (!logits || !labels || !loss || !grad) return fail(CE_EINVAL, "null xent operand");
+  if (n < 1 || n > 1024 || k < 1) return fail(CE_EINVAL, "xent supports 1 <= n <= 1024 rows (got n=%d k=%d)", n, k);
+  xent_kernel<int64_t><<<1, 1024, 0, (cudaStream_t)stream>>>(logits, labels, n, k, grad, loss, nullptr, nullptr);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+int ce_sgd_momentum(float* w, float* vel, const float* g, size_t count, float lr, float momentum, void* stream) {
+  if (!(lr > 0.f)) return fail(CE_EINVAL, "lr must be positive, got %g", (double)lr);
+  if (!(momentum >= 0.f && momentum < 1.f)) return fail(CE_EINVAL, "momentum must lie in [0, 1), got %g", (double)momentum);
+  if (count == 0) return CE_OK;
+  if (!w || !vel || !g) return fail(CE_EINVAL, "null sgd operand");
+  sgd_momentum_kernel<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(w, vel, g, count, lr, momentum);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+int ce_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t skip,
+                     double low, double high, float* out, size_t count, void* stream) {
+  if (count == 0) return CE_OK;
+  if (!out) return fail(CE_EINVAL, "null output");
+  InitLayout L{};
+  L.kind = 0;
+  const size_t nchunks = (count + kInitChunk - 1) / kInitChunk;
+  kaiming_uniform_kernel<<<grid_for(nchunks, 128), 128, 0, (cudaStream_t)stream>>>(
+      state_hi, state_lo, inc_hi, inc_lo, (unsigned long long)skip, count, low, high - low, L, out);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+int ce_permute_flatten_weights(const float* src, size_t rows, int c, int c_store, int hw, int direction, float* dst,
+                               void* stream) {
+  if (!src || !dst || c < 1 || c_store < c || hw < 1) return fail(CE_EINVAL, "bad permute arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (direction == 0)
+    dense_w_to_dev_kernel<<<grid_for(rows * hw * c_store), 256, 0, st>>>(src, rows, c, c_store, hw, dst);
+  else if (direction == 1)
+    dense_w_to_host_kernel<<<grid_for(rows * hw * c), 256, 0, st>>>(src, rows, c, c_store, hw, dst);
+  else
+    return fail(CE_EINVAL, "direction must be 0 or 1");
   CE_CHECK_LAUNCH();
   return CE_OK;
 }

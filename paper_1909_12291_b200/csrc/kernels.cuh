@@ -448,6 +448,7 @@ struct DenseSgdEpi {
   __device__ void operator()(int o, int i, int, float g) const {
     size_t off = (size_t)o * in + i;
     if (gw) gw[off] = g;
+    if (!w) return;  // gradient only
     float wv = w[off], vv = vel[off];
     sgd_update(wv, vv, g, lr, mu);
     w[off] = wv;
@@ -460,7 +461,7 @@ struct DenseSgdEpi {
   __device__ Pre prefetch4(int o, int i, int cnt) const {
     const size_t off = (size_t)o * in + i;
     Pre p;
-    if (cnt == 4 && (off & 3) == 0) {
+    if (w && cnt == 4 && (off & 3) == 0) {
       p.w = *(const float4*)(w + off);
       p.v = *(const float4*)(vel + off);
     }
@@ -468,6 +469,11 @@ struct DenseSgdEpi {
   }
   __device__ void commit4(int o, int i, const float* g, int cnt, Pre p) const {
     const size_t off = (size_t)o * in + i;
+    if (!w) {
+      if (cnt == 4 && (off & 3) == 0) *(float4*)(gw + off) = make_float4(g[0], g[1], g[2], g[3]);
+      else for (int j = 0; j < cnt; ++j) gw[off + j] = g[j];
+      return;
+    }
     if (cnt == 4 && (off & 3) == 0) {
       if (gw) *(float4*)(gw + off) = make_float4(g[0], g[1], g[2], g[3]);
       sgd_update(p.w.x, p.v.x, g[0], lr, mu);

@@ -431,7 +431,7 @@ int enqueue_step(ce_net* net, int n, float lr, float mu) {
   const Layer& last = net->L.back();
   {
     Prof pf(net, P_LOSS, 0.0, 16.0 * n * net->classes);
-    xent_kernel<<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes,
+    xent_kernel<int32_t><<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes,
                                           (float*)net->gbuf[0], net->d_losses, net->d_step, net->d_step + 1);
     CE_CHECK_LAUNCH();
   }
@@ -840,7 +840,8 @@ int ce_net_init_uniform(ce_net* net, int p, uint64_t st_hi, uint64_t st_lo, uint
   }
   CE_CUDA(cudaMemsetAsync(l.W, 0, l.wn * 4, st));
   const size_t nchunks = (count + kInitChunk - 1) / kInitChunk;
-  kaiming_uniform_kernel<<<grid_for(nchunks, 128), 128, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, count, limit, L, l.W);
+  kaiming_uniform_kernel<<<grid_for(nchunks, 128), 128, 0, st>>>(st_hi, st_lo, inc_hi, inc_lo, 0ull, count,
+                                                                  -limit, 2.0 * limit, L, l.W);
   CE_CHECK_LAUNCH();
   CE_CUDA(cudaMemsetAsync(l.b, 0, l.bn * 4, st));
   CE_CUDA(cudaMemsetAsync(l.VW, 0, l.wn * 4, st));

@@ -26,10 +26,12 @@ __global__ void gather_u8_kernel(const uint8_t* __restrict__ pix, const uint8_t*
                                  int32_t* __restrict__ y) {
   const int b = blockIdx.y;
   int src;
-  if (perm) {
+  if (perm && step_ctr) {
     const int step = *step_ctr;
     const int epoch = step / steps_per_epoch, bi = step - epoch * steps_per_epoch;
     src = perm[(size_t)epoch * n_perm + (size_t)bi * B + b];
+  } else if (perm) {  // plain index list (kernel-level ABI)
+    src = perm[base + b];
   } else {
     src = base + b;
   }
@@ -41,7 +43,7 @@ __global__ void gather_u8_kernel(const uint8_t* __restrict__ pix, const uint8_t*
       stf(dst, c, v);
     }
   }
-  if (y && blockIdx.x == 0 && threadIdx.x == 0) y[b] = labels[src];
+  if (y && labels && blockIdx.x == 0 && threadIdx.x == 0) y[b] = labels[src];
 }
 
 // fp32 NCHW (host batch) -> T NHWC padded
@@ -357,13 +359,13 @@ __global__ void dense_reduce_kernel(const float* __restrict__ part, int splits, 
     const size_t e = blockIdx.x * (size_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
     if (e >= total) return;
     const float acc = warp_sum_splits(part, splits, total, e);
-    if ((threadIdx.x & 31) == 0) y[e] = acc + bias[e % out];
+    if ((threadIdx.x & 31) == 0) y[e] = acc + (bias ? bias[e % out] : 0.f);
     return;
   }
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     float acc = 0.f;
     for (int s = 0; s < splits; ++s) acc += part[(size_t)s * total + e];
-    y[e] = acc + bias[e % out];
+    y[e] = acc + (bias ? bias[e % out] : 0.f);
   }
 }
 inline void launch_dense_reduce(const float* part, int splits, int B, int out, const float* bias, float* y,
@@ -379,7 +381,10 @@ inline void launch_dense_reduce(const float* part, int splits, int B, int out, c
 // softmax cross-entropy (nn.py:287-303), one block, B <= 1024:
 // loss = -mean(logp[label]); grad = (softmax - onehot) / B.
 // Writes losses[*step] and advances the step counter (end of the step).
-__global__ void xent_kernel(const float* __restrict__ logits, const int32_t* __restrict__ y, int B, int K,
+// Without a step counter the loss goes to losses[0] (kernel-level ABI); a label
+// outside [0, K) makes the loss NaN.
+template <class TL>
+__global__ void xent_kernel(const float* __restrict__ logits, const TL* __restrict__ y, int B, int K,
                             float* __restrict__ grad, float* __restrict__ losses, int* __restrict__ step_ctr,
                             int* __restrict__ nonfinite) {
   __shared__ double red[1024];
@@ -392,7 +397,8 @@ __global__ void xent_kernel(const float* __restrict__ logits, const int32_t* __r
     float se = 0.f;
     for (int k = 0; k < K; ++k) se += expf(z[k] - mx);
     float lse = logf(se);
-    const int lab = y[b];
+    const long long lab = (long long)y[b];
+    if (lab < 0 || lab >= K) lp = __longlong_as_double(0x7ff8000000000000ll);
     for (int k = 0; k < K; ++k) {
       float logp = (z[k] - mx) - lse;
       float gk = expf(logp);
@@ -410,11 +416,11 @@ __global__ void xent_kernel(const float* __restrict__ logits, const int32_t* __r
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const int step = *step_ctr;
+    const int step = step_ctr ? *step_ctr : 0;
     const float loss = (float)(-red[0] / B);
     losses[step] = loss;
     if (nonfinite && !isfinite(loss)) *nonfinite = 1;  // host stops replaying (evaluator.py:168-170)
-    *step_ctr = step + 1;
+    if (step_ctr) *step_ctr = step + 1;
   }
 }
 

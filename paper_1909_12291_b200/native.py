@@ -35,6 +35,14 @@ class ConvDesc(C.Structure):
                 ("kernel", C.c_int), ("stride", C.c_int), ("precision", C.c_int)]
 
 
+class DenseDesc(C.Structure):
+    _fields_ = [("n", C.c_int), ("in_units", C.c_int), ("out_units", C.c_int), ("precision", C.c_int)]
+
+
+class SgdArgs(C.Structure):
+    _fields_ = [("lr", C.c_float), ("momentum", C.c_float), ("vel_w", C.c_void_p), ("vel_b", C.c_void_p)]
+
+
 _P = C.c_void_p
 _F = C.POINTER(C.c_float)
 _D = C.POINTER(C.c_double)
@@ -69,6 +77,16 @@ _SIGNATURES = {
     "ce_conv_wgrad": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "ce_maxpool_fwd": ([C.POINTER(ConvDesc), _P, _P, _P, _P], C.c_int),
     "ce_maxpool_bwd": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P], C.c_int),
+    "ce_gather_u8_normalize": ([_P, C.c_int, C.c_int, C.c_int, _P, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
+    "ce_dense_workspace_bytes": ([C.POINTER(DenseDesc)], C.c_size_t),
+    "ce_dense_fwd": ([C.POINTER(DenseDesc), _P, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "ce_dense_bwd": ([C.POINTER(DenseDesc), _P, _P, _P, _P, _P, _P, _P, _P, _P, C.POINTER(SgdArgs), _P,
+                      C.c_size_t, _P], C.c_int),
+    "ce_softmax_xent": ([_P, _P, C.c_int, C.c_int, _P, _P, _P], C.c_int),
+    "ce_sgd_momentum": ([_P, _P, _P, C.c_size_t, C.c_float, C.c_float, _P], C.c_int),
+    "ce_pcg64_uniform": ([C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_double, _P,
+                          C.c_size_t, _P], C.c_int),
+    "ce_permute_flatten_weights": ([_P, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
     "ce_launch_count": ([], C.c_longlong),
     "ce_prof_num_classes": ([], C.c_int),
     "ce_net_set_profiling": ([_P, C.c_int], C.c_int),
@@ -140,6 +158,47 @@ def maxpool_fwd(desc, x, y, arg, stream=0):
 
 def maxpool_bwd(desc, dy, arg, mask, dx, stream=0):
     check(load().ce_maxpool_bwd(C.byref(desc), dy, arg, mask, dx, stream))
+
+
+def gather_u8_normalize(pixels, c, h, w, idx, n, c_store, precision, out, stream=0):
+    """Kernel-level batch gather + /255 normalise (device pointers)."""
+    check(load().ce_gather_u8_normalize(pixels, c, h, w, idx, n, c_store, PRECISIONS[precision], out, stream))
+
+
+def dense_desc(n, in_units, out_units, precision):
+    return DenseDesc(n, in_units, out_units, PRECISIONS[precision])
+
+
+def dense_workspace_bytes(desc):
+    return int(load().ce_dense_workspace_bytes(C.byref(desc)))
+
+
+def dense_fwd(desc, x, w, w16, b, y, ws, ws_bytes, stream=0):
+    check(load().ce_dense_fwd(C.byref(desc), x, w, w16, b, y, ws, ws_bytes, stream))
+
+
+def dense_bwd(desc, x, dy, w, w16, b, dx, mask, dw, db, sgd, ws, ws_bytes, stream=0):
+    """sgd: None or (lr, momentum, vel_w_ptr, vel_b_ptr) for the fused update."""
+    args = None if sgd is None else C.byref(SgdArgs(sgd[0], sgd[1], sgd[2], sgd[3]))
+    check(load().ce_dense_bwd(C.byref(desc), x, dy, w, w16, b, dx, mask, dw, db, args, ws, ws_bytes, stream))
+
+
+def softmax_xent(logits, labels, n, k, loss, grad, stream=0):
+    check(load().ce_softmax_xent(logits, labels, n, k, loss, grad, stream))
+
+
+def sgd_momentum(w, vel, g, count, lr, momentum, stream=0):
+    check(load().ce_sgd_momentum(w, vel, g, count, lr, momentum, stream))
+
+
+def pcg64_uniform(state, inc, skip, low, high, out, count, stream=0):
+    """numpy PCG64(state, inc) advanced by `skip`, .uniform(low, high, count) as float32 into device `out`."""
+    m = (1 << 64) - 1
+    check(load().ce_pcg64_uniform(state >> 64, state & m, inc >> 64, inc & m, skip, low, high, out, count, stream))
+
+
+def permute_flatten_weights(src, rows, c, c_store, hw, direction, dst, stream=0):
+    check(load().ce_permute_flatten_weights(src, rows, c, c_store, hw, direction, dst, stream))
 
 
 def launch_count():
