@@ -17,7 +17,19 @@
  *   ce_net_get_params                   <- Layer.params / Layer._vel after sgd_step (nn.py:306-322)
  *   ce_predict                          <- evaluator.predict_scores  (evaluator.py:174-186)
  *   ce_latency                          <- evaluator.measure_latency (evaluator.py:189-210)
+ *   ce_predict_stream                   <- predict_scores over a streamed slide + metrics.slide_seconds
+ *                                          (evaluator.py:174-186, metrics.py:77-81)
  *   ce_dataset_create                   <- data.PatchSet.as_float    (data.py:65-66), uploaded once
+ *
+ * Kernel level (operator drop-in, paper_1909_12291_b200/nn.py):
+ *   ce_conv_fwd / ce_conv_wgrad / ce_conv_dgrad  <- Conv2d.forward / backward (nn.py:82-116)
+ *   ce_maxpool_fwd / ce_maxpool_bwd              <- MaxPool.forward / backward (nn.py:140-167)
+ *   ce_dense_fwd / ce_dense_bwd                  <- Dense.forward / backward   (nn.py:225-240)
+ *   ce_softmax_xent                              <- softmax_cross_entropy      (nn.py:287-303)
+ *   ce_sgd_momentum                              <- sgd_step, per tensor       (nn.py:306-322)
+ *   ce_pcg64_uniform                             <- _kaiming_uniform draws     (nn.py:44-46)
+ *   ce_gather_u8_normalize                       <- PatchSet.as_float + x[idx] (data.py:65-66, evaluator.py:166)
+ *   ce_permute_flatten_weights                   <- Flatten column order       (nn.py:186-202)
  *
  * Conventions
  *   - Every entry point returns a status (CE_OK ... CE_ECUDA); the message of
@@ -124,6 +136,15 @@ int ce_train(ce_net* net, const ce_dataset* train, const int32_t* perm, int n_pe
              int steps_per_epoch, int batch, float lr, float momentum, float* losses, double* device_ms);
 /* predict_scores: softmax p[:,1] and argmax over the whole set in chunks of `batch` */
 int ce_predict(ce_net* net, const ce_dataset* set, int batch, double* scores, int64_t* preds);
+/* Streamed whole-slide inference: predict_scores (evaluator.py:174-186) over
+ * `count` u8 NCHW patches in HOST memory (pinned for full overlap; pageable
+ * input is page-locked for the call), copied in chunks of `batch` on a copy
+ * stream double-buffered against gather + forward + softmax head. scores
+ * (p[:,1]) / preds (argmax) go to host arrays of `count`; *seconds = device
+ * time from the first copy to the results on the host side of the last D2H
+ * (the prediction rate of metrics.py:77-81 is count / seconds).             */
+int ce_predict_stream(ce_net* net, const uint8_t* pixels, long long count, int batch, double* scores, int64_t* preds,
+                      double* seconds);
 /* measure_latency: warmup + reps device-timed forwards of a host batch (float32 NCHW) */
 int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double* seconds);
 

@@ -1094,6 +1094,97 @@ int ce_predict(ce_net* net, const ce_dataset* ds, int batch, double* scores, int
   return CE_OK;
 }
 
+namespace {
+// RAII for the streaming resources of ce_predict_stream
+struct StreamRes {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev[6] = {};
+  uint8_t* stage[2] = {};
+  cudaStream_t owner = nullptr;
+  const void* registered = nullptr;
+  ~StreamRes() {
+    if (owner) {
+      cudaStreamSynchronize(owner);
+      for (auto* p : stage)
+        if (p) cudaFreeAsync(p, owner);
+    }
+    if (cs) {
+      cudaStreamSynchronize(cs);
+      cudaStreamDestroy(cs);
+    }
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (registered) cudaHostUnregister(const_cast<void*>(registered));
+  }
+};
+}  // namespace
+
+int ce_predict_stream(ce_net* net, const uint8_t* pixels, long long count, int batch, double* scores, int64_t* preds,
+                      double* seconds) {
+  if (check_net(net)) return CE_EINVAL;
+  if (!pixels || count < 1 || batch < 1 || batch > net->max_batch || !scores || !preds)
+    return fail(CE_EINVAL, "ce_predict_stream: bad arguments");
+  DevGuard dg(net->device);
+  cudaStream_t st = net->st;
+  const int HW = net->in_h * net->in_w;
+  const size_t img = (size_t)net->in_c * HW;
+  const size_t total_bytes = img * (size_t)count;
+  if ((size_t)count > net->pred_cap) {
+    ALLOC(net->d_scores, (size_t)count * 8);
+    ALLOC(net->d_preds, (size_t)count * 8);
+    net->pred_cap = count;
+  }
+  StreamRes r;
+  // pageable input is page-locked for the duration so the copies are truly async
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, pixels) != cudaSuccess || attr.type == cudaMemoryTypeUnregistered) {
+    cudaGetLastError();
+    CE_CUDA(cudaHostRegister(const_cast<uint8_t*>(pixels), total_bytes, cudaHostRegisterReadOnly));
+    r.registered = pixels;
+  }
+  CE_CUDA(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking));
+  for (auto& e : r.ev) CE_CUDA(cudaEventCreate(&e));
+  cudaEvent_t *copied = r.ev, *consumed = r.ev + 2, t0 = r.ev[4], t1 = r.ev[5];
+  r.owner = st;
+  for (auto& p : r.stage) CE_CUDA(cudaMallocAsync((void**)&p, img * batch, st));
+  CE_CUDA(cudaEventRecord(t0, st));
+  CE_CUDA(cudaStreamWaitEvent(r.cs, t0, 0));  // staging exists, timing starts
+  net->acc = 0;
+  const long long chunks = (count + batch - 1) / batch;
+  for (long long i = 0; i < chunks; ++i) {
+    const int b = (int)(i & 1);
+    const long long start = i * batch;
+    const int nb = (int)std::min<long long>(batch, count - start);
+    if (i >= 2) CE_CUDA(cudaStreamWaitEvent(r.cs, consumed[b], 0));  // gather of chunk i-2 done
+    CE_CUDA(cudaMemcpyAsync(r.stage[b], pixels + (size_t)start * img, img * nb, cudaMemcpyHostToDevice, r.cs));
+    CE_CUDA(cudaEventRecord(copied[b], r.cs));
+    CE_CUDA(cudaStreamWaitEvent(st, copied[b], 0));
+    dim3 grid(cdiv(HW, 256), nb);
+    if (net->prec == CE_PREC_FP32)
+      gather_u8_kernel<float><<<grid, 256, 0, st>>>(r.stage[b], nullptr, nullptr, nullptr, 0, 0, 0, nb, net->in_c,
+                                                    net->in_cp, HW, (float*)net->x0, nullptr);
+    else
+      gather_u8_kernel<bf16><<<grid, 256, 0, st>>>(r.stage[b], nullptr, nullptr, nullptr, 0, 0, 0, nb, net->in_c,
+                                                   net->in_cp, HW, (bf16*)net->x0, nullptr);
+    CE_CHECK_LAUNCH();
+    CE_CUDA(cudaEventRecord(consumed[b], st));  // the copy of chunk i+2 may now overwrite this buffer
+    if (int s = forward_any(net, nb)) return s;
+    predict_head_kernel<<<cdiv(nb, 128), 128, 0, st>>>((const float*)net->L.back().out, nb, net->classes, (int)start,
+                                                        net->d_scores, net->d_preds);
+    CE_CHECK_LAUNCH();
+    net->acc += 2;
+  }
+  g_launches += net->acc;
+  CE_CUDA(cudaMemcpyAsync(scores, net->d_scores, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+  CE_CUDA(cudaMemcpyAsync(preds, net->d_preds, (size_t)count * 8, cudaMemcpyDeviceToHost, st));
+  CE_CUDA(cudaEventRecord(t1, st));
+  CE_CUDA(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  CE_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  if (seconds) *seconds = ms * 1e-3;
+  return CE_OK;
+}
+
 int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double* seconds) {
   if (check_net(net)) return CE_EINVAL;
   if (n < 1 || n > net->max_batch || warmup < 0 || reps < 1) return fail(CE_EINVAL, "ce_latency: bad arguments");

@@ -71,6 +71,7 @@ _SIGNATURES = {
     "ce_train": ([_P, _P, _I32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float, _F, _D], C.c_int),
     "ce_predict": ([_P, _P, C.c_int, _D, _I64], C.c_int),
     "ce_latency": ([_P, _F, C.c_int, C.c_int, C.c_int, _D], C.c_int),
+    "ce_predict_stream": ([_P, _U8, C.c_longlong, C.c_int, _D, _I64, _D], C.c_int),
     "ce_conv_workspace_bytes": ([C.POINTER(ConvDesc)], C.c_size_t),
     "ce_conv_fwd": ([C.POINTER(ConvDesc), _P, _P, _P, C.c_int, _P, _P], C.c_int),
     "ce_conv_dgrad": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
@@ -332,6 +333,22 @@ class Net:
         check(load().ce_predict(self._h, dataset.handle, batch, scores.ctypes.data_as(_D),
                                 preds.ctypes.data_as(_I64)))
         return scores, preds
+
+    def predict_stream(self, pixels, batch=128):
+        """Streamed predict over host u8 NCHW patches; returns (scores, preds, device seconds)."""
+        n = len(pixels)
+        scores = np.empty(n, np.float64)
+        preds = np.empty(n, np.int64)
+        secs = C.c_double(0.0)
+        if isinstance(pixels, np.ndarray):
+            px = np.ascontiguousarray(pixels, dtype=np.uint8)
+            ptr = px.ctypes.data_as(_U8)
+        else:  # a (pinned) torch uint8 tensor on the host
+            px = pixels.contiguous()
+            ptr = C.cast(px.data_ptr(), _U8)
+        check(load().ce_predict_stream(self._h, ptr, n, batch, scores.ctypes.data_as(_D),
+                                       preds.ctypes.data_as(_I64), C.byref(secs)))
+        return scores, preds, secs.value
 
     def set_profiling(self, on):
         check(load().ce_net_set_profiling(self._h, int(bool(on))))

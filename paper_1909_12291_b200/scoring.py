@@ -100,6 +100,18 @@ class MetricsReport:
         payload.update(self.extras)
         return json.dumps(payload, sort_keys=True)
 
+    def to_text(self):
+        c = self.confusion
+        return "\n".join([
+            f"model:            {self.model_id}",
+            f"dataset:          {self.dataset_id}",
+            f"f1 (positive):    {self.f1:.4f}" + ("  [degenerate]" if self.f1_degenerate else ""),
+            f"auc:              {self.auc:.4f}",
+            f"confusion:        tp={c['tp']} fp={c['fp']} fn={c['fn']} tn={c['tn']}",
+            f"prediction rate:  {self.prediction_rate_patches_per_s:.1f} patches/s",
+            f"est. slide time:  {slide_seconds(self.prediction_rate_patches_per_s):.1f} s (200000 patches)",
+        ])
+
 
 # --------------------------------------------------------------------------
 # fitness (fitness.py:12-82)
