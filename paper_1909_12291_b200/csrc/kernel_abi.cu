@@ -5,6 +5,7 @@
 #include "ops.cuh"
 #include "conv_tc.cuh"
 #include "dense_tc.cuh"
+#include "dense_simt.cuh"
 #include "init.cuh"
 
 using namespace ce;
@@ -267,7 +268,10 @@ int ce_dense_bwd(const ce_dense_desc* d, const void* x, const float* dy, float* 
                               st))
         return s;
     }
-    if (sgd || dw) {
+    if ((sgd || dw) && dense_dw_simt_enabled(n)) {
+      dense_dw_sgd_simt((const bf16*)x, in_pad, dy, n, in, out, sgd ? w : nullptr, sgd ? sgd->vel_w : nullptr, dw,
+                        sgd ? (bf16*)w16 : nullptr, in_pad, lr, mu, st);
+    } else if (sgd || dw) {
       if (int s = dense_dw_sgd_tc((const bf16*)x, in_pad, gbf, in, in_pad, out, out_pad, n, sgd ? w : nullptr,
                                   sgd ? sgd->vel_w : nullptr, dw, sgd ? (bf16*)w16 : nullptr, lr, mu, sms(), st))
         return s;
@@ -275,10 +279,16 @@ int ce_dense_bwd(const ce_dense_desc* d, const void* x, const float* dy, float* 
   } else {
     if (!w && dx) return fail(CE_EINVAL, "null dense weights");
     bpart = (float*)workspace;
-    if (dx)
+    const bool small = n <= kDenseSimtMaxBatch;
+    if (dx && small)
+      dense_dx_simt(dy, w, n, in, out, (const float*)mask, (float*)dx, st);
+    else if (dx)
       simt_gemm(DenseGA{dy, out}, DenseWN{w, in}, DenseDxEpi<float, float>{(float*)dx, (const float*)mask, in}, n, in,
                 out, 1, st);
-    if (sgd || dw) {
+    if ((sgd || dw) && small) {
+      dense_dw_sgd_simt((const float*)x, in, dy, n, in, out, sgd ? w : nullptr, sgd ? sgd->vel_w : nullptr, dw,
+                        (bf16*)nullptr, 0, lr, mu, st);
+    } else if (sgd || dw) {
       DenseSgdEpi se{sgd ? w : nullptr, sgd ? sgd->vel_w : nullptr, dw, nullptr, in, lr, mu};
       simt_gemm(DenseGT{dy, out}, DenseXN<float>{(const float*)x, in}, se, out, in, n, 1, st);
     }

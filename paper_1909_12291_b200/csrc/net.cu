@@ -16,6 +16,7 @@
 #include "ops.cuh"
 #include "conv_tc.cuh"
 #include "dense_tc.cuh"
+#include "dense_simt.cuh"
 #include "init.cuh"
 
 namespace ce {
@@ -330,8 +331,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
               (l.need_dx ? 24.0 : 20.0) * K * O + 2.0 * (l.in_is_act ? act_bytes(net) : 4.0) * B * K,
               l.need_dx ? 4 : 3);
       if (net->use_tc) {
-        f32_to_bf16_pad_kernel<<<grid_for((size_t)B * l.out_pad), 256, 0, st>>>(g, B, O, l.out_pad, net->gbf);
-        CE_CHECK_LAUNCH();
+        const bool dw_simt = dense_dw_simt_enabled(B);
+        if (l.need_dx || !dw_simt) {
+          f32_to_bf16_pad_kernel<<<grid_for((size_t)B * l.out_pad), 256, 0, st>>>(g, B, O, l.out_pad, net->gbf);
+          CE_CHECK_LAUNCH();
+        }
         if (l.need_dx) {
           int s = l.in_is_act ? dense_dx_tc(l.Wbp, net->gbf, K, l.in_pad, O, l.out_pad, B, mask, (T*)gout,
                                             net->num_sms, st)
@@ -340,23 +344,44 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
           if (s != CE_OK) return s;
         }
         const bf16* xb = l.in_is_act ? (const bf16*)x : l.x16;
-        int s = dense_dw_sgd_tc(xb, l.in_pad, net->gbf, K, l.in_pad, O, l.out_pad, B, l.W, l.VW, keep ? l.GW : nullptr,
-                                l.Wbp, lr, mu, net->num_sms, st);
-        if (s != CE_OK) return s;
+        if (dw_simt) {
+          dense_dw_sgd_simt(xb, l.in_pad, g, B, K, O, l.W, l.VW, keep ? l.GW : nullptr, l.Wbp, l.in_pad, lr, mu, st);
+          CE_CHECK_LAUNCH();
+        } else {
+          int s = dense_dw_sgd_tc(xb, l.in_pad, net->gbf, K, l.in_pad, O, l.out_pad, B, l.W, l.VW,
+                                  keep ? l.GW : nullptr, l.Wbp, lr, mu, net->num_sms, st);
+          if (s != CE_OK) return s;
+        }
       } else {
+      const bool small = B <= kDenseSimtMaxBatch;
       if (l.need_dx) {
-        if (l.in_is_act)
+        if (small) {
+          if (l.in_is_act)
+            dense_dx_simt(g, l.W, B, K, O, mask, (T*)gout, st);
+          else
+            dense_dx_simt(g, l.W, B, K, O, (const float*)nullptr, (float*)gout, st);
+        } else if (l.in_is_act) {
           simt_gemm(DenseGA{g, O}, DenseWN{l.W, K}, DenseDxEpi<T, T>{(T*)gout, mask, K}, B, K, O, 1, st);
-        else
+        } else {
           simt_gemm(DenseGA{g, O}, DenseWN{l.W, K}, DenseDxEpi<float, float>{(float*)gout, nullptr, K}, B, K, O, 1,
                     st);
+        }
         CE_CHECK_LAUNCH();
       }
-      DenseSgdEpi se{l.W, l.VW, keep ? l.GW : nullptr, nullptr, K, lr, mu};
-      if (l.in_is_act)
-        simt_gemm(DenseGT{g, O}, DenseXN<T>{(const T*)x, K}, se, O, K, B, 1, st);
-      else
-        simt_gemm(DenseGT{g, O}, DenseXN<float>{(const float*)x, K}, se, O, K, B, 1, st);
+      if (small) {
+        if (l.in_is_act)
+          dense_dw_sgd_simt((const T*)x, K, g, B, K, O, l.W, l.VW, keep ? l.GW : nullptr, (bf16*)nullptr, 0, lr, mu,
+                            st);
+        else
+          dense_dw_sgd_simt((const float*)x, K, g, B, K, O, l.W, l.VW, keep ? l.GW : nullptr, (bf16*)nullptr, 0, lr,
+                            mu, st);
+      } else {
+        DenseSgdEpi se{l.W, l.VW, keep ? l.GW : nullptr, nullptr, K, lr, mu};
+        if (l.in_is_act)
+          simt_gemm(DenseGT{g, O}, DenseXN<T>{(const T*)x, K}, se, O, K, B, 1, st);
+        else
+          simt_gemm(DenseGT{g, O}, DenseXN<float>{(const float*)x, K}, se, O, K, B, 1, st);
+      }
       CE_CHECK_LAUNCH();
       }
       float* bpart = net->ws;
