@@ -248,10 +248,13 @@ def main():
     mine = shard_lpt(genomes, world, lambda g: estimate_cost(g, n_train, budget))[rank]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
+    last_trace = []
+
     def step(profile=False):
-        recs, _ = evaluate_population(mine, splits, budget, obj, seed=0, devices=(device,),
-                                      slots_per_gpu=1 if profile else args.slots, precision=args.precision,
-                                      profile=profile)
+        recs, report = evaluate_population(mine, splits, budget, obj, seed=0, devices=(device,),
+                                           slots_per_gpu=1 if profile else args.slots, precision=args.precision,
+                                           profile=profile)
+        last_trace[:] = getattr(report, "trace", [])
         return recs
 
     def timed(n_steps, e2e=False):
@@ -280,6 +283,12 @@ def main():
     clocks.start()
     times, launches, recs = timed(args.steps)
     clock_info = clocks.stop()
+    if os.environ.get("BENCH_TRACE"):  # per-candidate timeline of the last timed step (stderr)
+        t0 = min(t[2] for t in last_trace)
+        idx = {g.id: i for i, g in enumerate(mine)}
+        for gid, wid, a, b in sorted(last_trace, key=lambda t: t[2]):
+            print(f"trace {wid} g{idx.get(gid, -1):02d} start {1000 * (a - t0):8.1f} ms  dur {1000 * (b - a):8.1f} ms",
+                  file=sys.stderr)
     ms = allreduce([statistics.fmean(times)])[0]
     launches = int(allreduce([launches], "sum")[0])
     total_candidates = POP_PER_GPU * world
@@ -295,7 +304,8 @@ def main():
             "train_img_per_s": train_imgs / (ms * 1e-3),
             "candidates_ok": int(allreduce([ok], "sum")[0]),
             "failures": [r.failure_reason[:120] for r in recs if r is not None and not r.ok],
-            "gpu_launches": launches, "clocks": clock_info}
+            "gpu_launches": launches, "clocks": clock_info,
+            "step_ms": [round(t, 1) for t in times]}
 
     if not args.no_e2e:
         e_times, _, _ = timed(max(1, args.steps), e2e=True)

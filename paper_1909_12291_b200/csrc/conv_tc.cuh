@@ -580,6 +580,39 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
   });
 }
 
+// Auxiliary streams for independent launches of one layer pass (the stride^2
+// dgrad classes): fork from the caller's stream with an event, join back
+// with one event per branch. Per calling thread and device (a worker thread
+// drives one net at a time); under graph capture the branches become
+// parallel graph nodes. CE_SERIAL_CLASSES=1 keeps everything on one stream.
+struct ForkStreams {
+  static constexpr int N = 8;
+  cudaStream_t aux[N] = {};
+  cudaEvent_t done[N] = {};
+  cudaEvent_t start = nullptr;
+  int device = -1;
+};
+inline ForkStreams* fork_streams() {
+  static const bool serial = [] {
+    const char* e = getenv("CE_SERIAL_CLASSES");
+    return e && e[0] == '1';
+  }();
+  if (serial) return nullptr;
+  thread_local ForkStreams fs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (fs.device != dev) {
+    for (int i = 0; i < ForkStreams::N; ++i) {
+      if (cudaStreamCreateWithFlags(&fs.aux[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&fs.done[i], cudaEventDisableTiming) != cudaSuccess)
+        return nullptr;
+    }
+    if (cudaEventCreateWithFlags(&fs.start, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    fs.device = dev;
+  }
+  return &fs;
+}
+
 inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, const bf16* mask, bf16* dx, int num_sms,
                          cudaStream_t st) {
   bool any_empty = false;
@@ -590,8 +623,21 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
     cudaError_t e = cudaMemsetAsync(dx, 0, (size_t)g.n * g.h * g.w * g.c * sizeof(bf16), st);
     if (e != cudaSuccess) return fail(CE_ECUDA, "conv_dgrad_tc memset: %s", cudaGetErrorString(e));
   }
+  int n_cls = 0;
+  for (int rh = 0; rh < g.s && rh < g.h; ++rh)
+    for (int rw = 0; rw < g.s && rw < g.w; ++rw)
+      if (rh < g.k && rw < g.k) ++n_cls;
+  ForkStreams* fs = n_cls > 1 ? fork_streams() : nullptr;
+  if (fs && cudaEventRecord(fs->start, st) != cudaSuccess) return fail(CE_ECUDA, "conv_dgrad_tc: fork");
+  int ci = 0;
+  const cudaStream_t home = st;
   for (int rh = 0; rh < g.s && rh < g.h; ++rh)
     for (int rw = 0; rw < g.s && rw < g.w; ++rw) {
+      if (rh >= g.k || rw >= g.k) continue;
+      st = (fs && ci > 0) ? fs->aux[ci - 1] : home;
+      if (st != home && cudaStreamWaitEvent(st, fs->start, 0) != cudaSuccess)
+        return fail(CE_ECUDA, "conv_dgrad_tc: fork wait");
+      ++ci;
       DgradClass cl;
       cl.rh = rh;
       cl.rw = rw;
@@ -636,6 +682,11 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
       });
       if (s != CE_OK) return s;
     }
+  if (fs)  // join every branch back into the caller's stream
+    for (int b = 1; b < ci; ++b)
+      if (cudaEventRecord(fs->done[b - 1], fs->aux[b - 1]) != cudaSuccess ||
+          cudaStreamWaitEvent(home, fs->done[b - 1], 0) != cudaSuccess)
+        return fail(CE_ECUDA, "conv_dgrad_tc: join");
   return CE_OK;
 }
 

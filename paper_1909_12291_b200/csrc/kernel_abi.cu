@@ -151,9 +151,8 @@ int ce_conv_wgrad(const ce_conv_desc* d, const void* x, const void* dy, float* d
   CE_CHECK_LAUNCH();
   float* bpart = part + (size_t)splits * g.co * K;
   const int bsplits = tc ? colsum((const bf16*)dy, Mo, g.co, bpart, st) : colsum((const float*)dy, Mo, g.co, bpart, st);
-  conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(part, splits, g.co, K, g.c, g.k, g.s, nullptr, nullptr,
-                                                               dw, nullptr, nullptr, 0.f, 0.f);
-  launch_bias_sgd(bpart, bsplits, g.co, nullptr, nullptr, db, 0.f, 0.f, st);
+  launch_conv_sgd(part, splits, g.co, K, g.c, g.k, g.s, nullptr, nullptr, dw, nullptr, nullptr, bpart, bsplits, nullptr,
+                  nullptr, db, 0.f, 0.f, st);
   CE_CHECK_LAUNCH();
   return CE_OK;
 }

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include "ops.cuh"
 #include "conv_tc.cuh"
 #include "dense_tc.cuh"
@@ -141,6 +143,65 @@ int dev_alloc(ce_net* net, void** p, size_t bytes) {
     int s_ = dev_alloc(net, (void**)&(ptr), (bytes));                 \
     if (s_ != CE_OK) return s_;                                       \
   } while (0)
+
+// Per-device execution gate (latency is measured in an
+// exclusive per-GPU window). Candidate work on a device -- each ce_train replay
+// chunk, predict, forward, parameter upload -- holds the gate shared and
+// releases it only after that work has completed (or, for the train loop,
+// with at most one chunk in flight, which ce_latency drains with a device
+// synchronize). ce_latency holds it exclusively; a waiting measurement blocks
+// new shared entries (writer preference), so it waits at most one chunk per
+// concurrent slot. Only the library's own entry points take the gate; it is
+// never taken twice on one thread.
+struct DeviceGate {
+  std::mutex m;
+  std::condition_variable cv;
+  int readers = 0, writers_waiting = 0;
+  bool writer = false;
+  void lock_shared() {
+    std::unique_lock<std::mutex> l(m);
+    cv.wait(l, [&] { return !writer && writers_waiting == 0; });
+    ++readers;
+  }
+  void unlock_shared() {
+    std::lock_guard<std::mutex> l(m);
+    if (--readers == 0) cv.notify_all();
+  }
+  void lock() {
+    std::unique_lock<std::mutex> l(m);
+    ++writers_waiting;
+    cv.wait(l, [&] { return !writer && readers == 0; });
+    --writers_waiting;
+    writer = true;
+  }
+  void unlock() {
+    std::lock_guard<std::mutex> l(m);
+    writer = false;
+    cv.notify_all();
+  }
+};
+constexpr int kMaxDevices = 64;
+DeviceGate g_gates[kMaxDevices];
+struct SharedGate {
+  DeviceGate* g;
+  explicit SharedGate(int dev) : g(dev >= 0 && dev < kMaxDevices ? &g_gates[dev] : nullptr) {
+    if (g) g->lock_shared();
+  }
+  ~SharedGate() { release(); }
+  void release() {
+    if (g) g->unlock_shared();
+    g = nullptr;
+  }
+};
+struct ExclusiveGate {
+  DeviceGate* g;
+  explicit ExclusiveGate(int dev) : g(dev >= 0 && dev < kMaxDevices ? &g_gates[dev] : nullptr) {
+    if (g) g->lock();
+  }
+  ~ExclusiveGate() {
+    if (g) g->unlock();
+  }
+};
 
 struct DevGuard {
   int prev = -1;
@@ -426,9 +487,8 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       float* bpart = net->ws + (size_t)splits * g.co * K;
       Prof pf(net, P_CONV_SGD, 0.0, ab * Mo * g.co + 4.0 * splits * g.co * K + 20.0 * g.co * K, 3);
       int bsplits = colsum(dy, Mo, g.co, bpart, st);
-      conv_sgd_kernel<<<grid_for((size_t)g.co * K), 256, 0, st>>>(net->ws, splits, g.co, K, g.c, g.k, g.s, l.W, l.VW,
-                                                                   keep ? l.GW : nullptr, l.Wbf, l.Wtbf, lr, mu);
-      launch_bias_sgd(bpart, bsplits, g.co, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu, st);
+      launch_conv_sgd(net->ws, splits, g.co, K, g.c, g.k, g.s, l.W, l.VW, keep ? l.GW : nullptr, l.Wbf, l.Wtbf, bpart,
+                      bsplits, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu, st);
       CE_CHECK_LAUNCH();
     } else {  // pool
       if (l.need_dx) {
@@ -804,6 +864,7 @@ int ce_net_set_params(ce_net* net, int p, const float* w, const float* b) {
   if (int s = param_layer(net, p, &lp)) return s;
   Layer& l = *lp;
   DevGuard dg(net->device);
+  SharedGate gate(net->device);
   cudaStream_t st = net->st;
   size_t hn = host_w_count(l);
   // stage through a temporary in chunks of rows to bound memory for giant heads
@@ -847,6 +908,7 @@ int ce_net_init_uniform(ce_net* net, int p, uint64_t st_hi, uint64_t st_lo, uint
   if (int s = param_layer(net, p, &lp)) return s;
   Layer& l = *lp;
   DevGuard dg(net->device);
+  SharedGate gate(net->device);
   cudaStream_t st = net->st;
   InitLayout L{};
   size_t count = host_w_count(l);
@@ -942,6 +1004,7 @@ int ce_net_forward_host(ce_net* net, const float* x, int n, float* logits) {
   if (check_net(net)) return CE_EINVAL;
   if (n < 1 || n > net->max_batch) return fail(CE_EINVAL, "batch %d outside [1, %d]", n, net->max_batch);
   DevGuard dg(net->device);
+  SharedGate gate(net->device);
   if (int s = upload_host_batch(net, x, n)) return s;
   if (int s = forward_any(net, n)) return s;
   if (logits)
@@ -983,6 +1046,7 @@ int ce_net_train_batch_host(ce_net* net, const float* x, const int64_t* labels, 
   if (check_net(net)) return CE_EINVAL;
   if (n < 1 || n > net->max_batch) return fail(CE_EINVAL, "batch %d outside [1, %d]", n, net->max_batch);
   DevGuard dg(net->device);
+  SharedGate gate(net->device);
   std::vector<int32_t> y(n);
   for (int i = 0; i < n; ++i) {
     if (labels[i] < 0 || labels[i] >= net->classes) return fail(CE_EINVAL, "labels must lie in [0, %d]", net->classes - 1);
@@ -1030,6 +1094,7 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   bool graphed = false;
   net->acc = 0;
   long long per_step = 0;
+  SharedGate capture_gate(net->device);  // no exclusive latency window (device sync) during a capture
   if (!net->prof_on && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
     int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true);
     if (s == CE_OK) s = step_any(net, batch, lr, momentum);
@@ -1042,6 +1107,7 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
     if (graph) cudaGraphDestroy(graph);
     per_step = net->acc;
   }
+  capture_gate.release();
   cudaGetLastError();
   net->acc = 0;
   cudaEvent_t e0, e1, chunk_ev[2];
@@ -1057,12 +1123,15 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   int launched = 0, nchunk = 0;
   while (launched < steps) {
     const int todo = std::min(chunk, steps - launched);
-    for (int i = 0; i < todo; ++i) {
-      if (graphed) {
-        CE_CUDA(cudaGraphLaunch(exec, st));
-      } else {
-        if (int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true)) return s;
-        if (int s = step_any(net, batch, lr, momentum)) return s;
+    {
+      SharedGate gate(net->device);  // enqueue under the gate; ce_latency drains in-flight chunks
+      for (int i = 0; i < todo; ++i) {
+        if (graphed) {
+          CE_CUDA(cudaGraphLaunch(exec, st));
+        } else {
+          if (int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true)) return s;
+          if (int s = step_any(net, batch, lr, momentum)) return s;
+        }
       }
     }
     launched += todo;
@@ -1096,6 +1165,7 @@ int ce_predict(ce_net* net, const ce_dataset* ds, int batch, double* scores, int
   if (check_net(net)) return CE_EINVAL;
   if (!ds || batch < 1 || batch > net->max_batch) return fail(CE_EINVAL, "ce_predict: bad arguments");
   DevGuard dg(net->device);
+  SharedGate gate(net->device);
   cudaStream_t st = net->st;
   if ((size_t)ds->n > net->pred_cap) {
     ALLOC(net->d_scores, (size_t)ds->n * 8);
@@ -1150,6 +1220,7 @@ int ce_predict_stream(ce_net* net, const uint8_t* pixels, long long count, int b
   if (!pixels || count < 1 || batch < 1 || batch > net->max_batch || !scores || !preds)
     return fail(CE_EINVAL, "ce_predict_stream: bad arguments");
   DevGuard dg(net->device);
+  SharedGate gate(net->device);
   cudaStream_t st = net->st;
   const int HW = net->in_h * net->in_w;
   const size_t img = (size_t)net->in_c * HW;
@@ -1214,6 +1285,10 @@ int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double*
   if (check_net(net)) return CE_EINVAL;
   if (n < 1 || n > net->max_batch || warmup < 0 || reps < 1) return fail(CE_EINVAL, "ce_latency: bad arguments");
   DevGuard dg(net->device);
+  // exclusive per-GPU window: no other slot enqueues while we hold the gate, and
+  // what they already enqueued drains before the first timed forward
+  ExclusiveGate gate(net->device);
+  CE_CUDA(cudaDeviceSynchronize());
   cudaStream_t st = net->st;
   net->acc = 0;
   if (int s = upload_host_batch(net, x, n)) return s;

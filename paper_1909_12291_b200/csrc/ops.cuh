@@ -15,6 +15,12 @@ inline int grid_for(size_t n, int threads = 256) {
   return (int)g;
 }
 
+// 8 consecutive elements <-> float[8] (16-byte bf16 / 2x16-byte fp32 vectors), defined below
+template <class T>
+__device__ __forceinline__ void load8(const T* p, float (&v)[8]);
+template <class T>
+__device__ __forceinline__ void store8(T* p, const float (&v)[8]);
+
 // ---------------------------------------------------------------- input
 // x[b][y][x][cp] = cp < C ? pix[idx[b]][cp][y][x] / 255 : 0      (data.py:65-66)
 // idx source: perm[epoch*n_perm + bi*B + b] with (epoch, bi) from the device
@@ -38,9 +44,15 @@ __global__ void gather_u8_kernel(const uint8_t* __restrict__ pix, const uint8_t*
   const uint8_t* img = pix + (size_t)src * C * HW;
   for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < HW; px += gridDim.x * blockDim.x) {
     T* dst = x + ((size_t)b * HW + px) * Cp;
-    for (int c = 0; c < Cp; ++c) {
-      float v = c < C ? __fdiv_rn((float)img[(size_t)c * HW + px], 255.0f) : 0.f;
-      stf(dst, c, v);
+    // 8 channels per vector store (Cp % 8 == 0): one 16-byte (bf16) / 2x16-byte (fp32) store
+    for (int c0 = 0; c0 < Cp; c0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u;
+        v[u] = c < C ? __fdiv_rn((float)img[(size_t)c * HW + px], 255.0f) : 0.f;
+      }
+      store8(dst + c0, v);
     }
   }
   if (y && labels && blockIdx.x == 0 && threadIdx.x == 0) y[b] = labels[src];
@@ -331,6 +343,146 @@ __device__ __forceinline__ float warp_sum_splits(const float* __restrict__ part,
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return acc;
 }
+
+// Tiled conv weight update: tile = 32 output channels x 64 reduction columns
+// (kk = (i, j, c)). Each thread owns 2 rows x 4 columns: split partials, W, V
+// and the bf16 mirror stream as float4 / 8-byte vectors along kk; the
+// dgrad-operand transpose Wt ([class][c][tap][o], o innermost) is staged in
+// shared memory and written as 16-byte rows of 8 output channels. Blocks of
+// the first column tile also reduce and apply the bias update (fixed split
+// order, deterministic). With w == null only the gradient is produced.
+constexpr int CS_TO = 32, CS_TK = 64;
+__device__ __forceinline__ float4 f4add(float4 a, const float4& b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  return a;
+}
+__global__ void __launch_bounds__(256) conv_sgd_tiled_kernel(
+    const float* __restrict__ part, int splits, int co, int K, int cp, int k, int s, float* __restrict__ w,
+    float* __restrict__ vel, float* __restrict__ gw, bf16* __restrict__ wbf, bf16* __restrict__ wtbf,
+    const float* __restrict__ bpart, int bsplits, float* __restrict__ b, float* __restrict__ vb,
+    float* __restrict__ gb, float lr, float mu) {
+  __shared__ __align__(16) bf16 tile[CS_TK][CS_TO + 8];
+  const int kq = threadIdx.x & 15, orow = threadIdx.x >> 4;
+  const int kk0 = blockIdx.x * CS_TK + kq * 4, o_base = blockIdx.y * CS_TO;
+  const size_t total = (size_t)co * K;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int o = o_base + orow + 16 * h;
+    if (o >= co || kk0 >= K) continue;
+    const size_t e = (size_t)o * K + kk0;
+    float4 g = *(const float4*)(part + e);
+    for (int sp = 1; sp < splits; ++sp) g = f4add(g, *(const float4*)(part + (size_t)sp * total + e));
+    if (gw) *(float4*)(gw + e) = g;
+    if (!w) continue;
+    float4 wv = *(const float4*)(w + e), vv = *(const float4*)(vel + e);
+    sgd_update(wv.x, vv.x, g.x, lr, mu);
+    sgd_update(wv.y, vv.y, g.y, lr, mu);
+    sgd_update(wv.z, vv.z, g.z, lr, mu);
+    sgd_update(wv.w, vv.w, g.w, lr, mu);
+    *(float4*)(w + e) = wv;
+    *(float4*)(vel + e) = vv;
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(wv.x, wv.y), hi = __floats2bfloat162_rn(wv.z, wv.w);
+    if (wbf) {
+      uint2 u;
+      u.x = *(const uint32_t*)&lo;
+      u.y = *(const uint32_t*)&hi;
+      *(uint2*)(wbf + e) = u;
+    }
+    const int ol = orow + 16 * h;
+    tile[kq * 4 + 0][ol] = lo.x;
+    tile[kq * 4 + 1][ol] = lo.y;
+    tile[kq * 4 + 2][ol] = hi.x;
+    tile[kq * 4 + 3][ol] = hi.y;
+  }
+  if (w && wtbf) {
+    __syncthreads();
+    // 64 columns x 4 chunks of 8 output channels: one 16-byte store each
+    const int kl = threadIdx.x >> 2, oc = (threadIdx.x & 3) * 8;
+    const int kk = blockIdx.x * CS_TK + kl, o = o_base + oc;
+    if (kk < K && o < co) {
+      const int c = kk % cp, tap = kk / cp;
+      const size_t dst = dg_wt_index(k, s, cp, co, tap / k, tap % k, c, o);
+      *(uint4*)(wtbf + dst) = *(const uint4*)&tile[kl][oc];
+    }
+  }
+  if (blockIdx.x == 0 && bpart) {  // bias of this tile's 32 channels: 8 warps x 4, warp-parallel over splits
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int oo = warp; oo < CS_TO; oo += 8) {
+      const int o = o_base + oo;
+      if (o >= co) break;
+      const float g = warp_sum_splits(bpart, bsplits, co, o);
+      if (lane == 0) {
+        if (gb) gb[o] = g;
+        if (b) {
+          float bv = b[o], v = vb[o];
+          sgd_update(bv, v, g, lr, mu);
+          b[o] = bv;
+          vb[o] = v;
+        }
+      }
+    }
+  }
+}
+// Many splits over a small layer: one warp per weight element, lanes take
+// strided splits and a fixed xor tree combines them (warp_sum_splits, deterministic);
+// block 0 also reduces and applies the bias update.
+__global__ void __launch_bounds__(256) conv_sgd_warp_kernel(
+    const float* __restrict__ part, int splits, int co, int K, int cp, int k, int s, float* __restrict__ w,
+    float* __restrict__ vel, float* __restrict__ gw, bf16* __restrict__ wbf, bf16* __restrict__ wtbf,
+    const float* __restrict__ bpart, int bsplits, float* __restrict__ b, float* __restrict__ vb,
+    float* __restrict__ gb, float lr, float mu) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const size_t total = (size_t)co * K;
+  const unsigned eblocks = (unsigned)((total + 7) / 8);
+  if (blockIdx.x >= eblocks) {  // trailing blocks: one warp per bias channel
+    const int o = (int)(blockIdx.x - eblocks) * 8 + warp;
+    if (!bpart || o >= co) return;
+    const float g = warp_sum_splits(bpart, bsplits, co, o);
+    if (lane == 0) {
+      if (gb) gb[o] = g;
+      if (b) {
+        float bv = b[o], v = vb[o];
+        sgd_update(bv, v, g, lr, mu);
+        b[o] = bv;
+        vb[o] = v;
+      }
+    }
+    return;
+  }
+  const size_t e = (size_t)blockIdx.x * 8 + warp;
+  if (e < total) {
+    const float g = warp_sum_splits(part, splits, total, e);
+    if (lane == 0) {
+      if (gw) gw[e] = g;
+      if (w) {
+        float wv = w[e], vv = vel[e];
+        sgd_update(wv, vv, g, lr, mu);
+        w[e] = wv;
+        vel[e] = vv;
+        if (wbf) wbf[e] = __float2bfloat16_rn(wv);
+        if (wtbf) {
+          const int o = (int)(e / K), kk = (int)(e % K), c = kk % cp, tap = kk / cp;
+          wtbf[dg_wt_index(k, s, cp, co, tap / k, tap % k, c, o)] = __float2bfloat16_rn(wv);
+        }
+      }
+    }
+  }
+}
+inline void launch_conv_sgd(const float* part, int splits, int co, int K, int cp, int k, int s, float* w, float* vel,
+                            float* gw, bf16* wbf, bf16* wtbf, const float* bpart, int bsplits, float* b, float* vb,
+                            float* gb, float lr, float mu, cudaStream_t st) {
+  if (splits > 16) {  // many splits = small layer: one warp per element
+    const size_t total = (size_t)co * K;
+    const unsigned blocks = (unsigned)((total + 7) / 8 + (co + 7) / 8);
+    conv_sgd_warp_kernel<<<blocks, 256, 0, st>>>(part, splits, co, K, cp, k, s, w, vel, gw, wbf, wtbf, bpart, bsplits,
+                                                 b, vb, gb, lr, mu);
+    return;
+  }
+  dim3 grid((K + CS_TK - 1) / CS_TK, (co + CS_TO - 1) / CS_TO);
+  conv_sgd_tiled_kernel<<<grid, 256, 0, st>>>(part, splits, co, K, cp, k, s, w, vel, gw, wbf, wtbf, bpart, bsplits, b,
+                                              vb, gb, lr, mu);
+}
+
 
 // bias: g = sum_split part[split][o]; one warp per output channel
 __global__ void bias_sgd_kernel(const float* __restrict__ part, int splits, int n, float* __restrict__ b,

@@ -76,6 +76,7 @@ def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), 
     pool = GpuPool(run_one, master, devices=devices, slots_per_gpu=slots_per_gpu, order=order,
                    cost_fn=lambda g: estimate_cost(g, n_train, budget))
     report = pool.run()
+    report.trace = pool.trace
     return [master.records.get(g.id) for g in master.genomes], report
 
 
