@@ -212,9 +212,41 @@ struct FwdTcLoader {
 };
 
 struct FwdTcEpi {
+  static constexpr bool STAGED_BF16 = true;  // coalesced row stores through shared memory (tc_engine)
   bf16* y;
   const float* bias;
   int M, co, relu;
+  // bias + ReLU of columns c.n0 + col .. +15 (row independent)
+  // out[i] = bf16x2 of columns 2i, 2i+1
+  __device__ void convert(const TileCoord& c, int col, const float (&v)[16], uint32_t (&out)[8]) const {
+    const int o0 = c.n0 + col;
+    float bv[16];
+    if (o0 + 16 <= co) {  // co % 8 == 0 and o0 % 16 == 0: 16-byte aligned
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float4 b4 = __ldg((const float4*)(bias + o0) + h);
+        bv[4 * h] = b4.x; bv[4 * h + 1] = b4.y; bv[4 * h + 2] = b4.z; bv[4 * h + 3] = b4.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) bv[i] = o0 + i < co ? __ldg(bias + o0 + i) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float t0 = v[2 * i] + bv[2 * i], t1 = v[2 * i + 1] + bv[2 * i + 1];
+      if (relu) {
+        t0 = t0 > 0.f ? t0 : 0.f;
+        t1 = t1 > 0.f ? t1 : 0.f;
+      }
+      const __nv_bfloat162 h = __floats2bfloat162_rn(t0, t1);
+      out[i] = *(const uint32_t*)&h;
+    }
+  }
+  // destination of the 8-column half `half` of row `row` at columns col.., or null
+  __device__ bf16* row_ptr(const TileCoord& c, int row, int col, int half) const {
+    const int m = c.m0 + row, o = c.n0 + col + half * 8;
+    return (m < M && o < co) ? y + (size_t)m * co + o : nullptr;
+  }
   __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
     const int m = c.m0 + row;
     const int o0 = c.n0 + col;

@@ -1,0 +1,224 @@
+// Packed first conv layer (tcgen05).
+//
+// The image layer stores 3 real channels padded to 8 (one 16-byte chunk per
+// pixel), so its implicit GEMMs run K = k*k*8 where only k*k*3 columns carry
+// data (k = 6: 288 vs 108). A conv whose input is channel-padded and that needs
+// no dX (the first parameterised layer) instead runs two plain GEMMs over an
+// explicit im2col matrix
+//     xcol[m][kk],  kk = (i*k + j)*c_real + c  for kk < Kr = k*k*c_real,
+//                   xcol[m][Kr] = 1, zero up to Kp = pad8(Kr + 1),
+// written once per forward (conv.forward, nn.py:82-94):
+//   forward  y = xcol . Wp^T      M = pixels, N = C_out, K = Kp  (pure 2D TMA)
+//   wgrad    D = xcol^T . dY      M = Kp, N = C_out, K = pixels  (2D TMA, split-K)
+// Row Kr of D is sum_pixels dY = the bias gradient (nn.py:115), so the
+// separate column-sum pass over dY disappears. Wp[o][kk] is the packed bf16
+// mirror of the fp32 master W[o][i][j][c_pad] (column Kr held at zero: the
+// bias is added in fp32 by the epilogue).
+#pragma once
+#include "conv_tc.cuh"
+#include "dense_tc.cuh"
+
+namespace ce {
+
+// CE_DISABLE_PACKED=1 runs the first layer through the padded implicit GEMMs (comparison)
+inline bool packed_disabled() {
+  static const bool off = [] {
+    const char* e = getenv("CE_DISABLE_PACKED");
+    return e && e[0] == '1';
+  }();
+  return off;
+}
+
+inline int packed_kr(const ConvGeom& g, int c_real) { return g.k * g.k * c_real; }
+inline int packed_kp(const ConvGeom& g, int c_real) { return (packed_kr(g, c_real) + 1 + 7) / 8 * 8; }
+
+// one thread per (pixel, 8-column chunk): 8 gathered bf16 -> one 16-byte store.
+// Column kk reads x at (receptive-field origin) + off[kk]; off is built once per
+// block in shared memory (-1: the ones column, -2: zero padding); index math
+// is 32-bit with magic-number division.
+constexpr int kPackedMaxKp = 1024;
+__global__ void __launch_bounds__(256) im2col_packed_kernel(const bf16* __restrict__ x, ConvGeom g, int c_real,
+                                                            int Kp, FastDiv d_chunks, FastDiv d_ow, FastDiv d_oh,
+                                                            bf16* __restrict__ xcol) {
+  __shared__ int off[kPackedMaxKp];
+  const int Kr = g.k * g.k * c_real;
+  for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
+    if (kk < Kr) {
+      const int tap = kk / c_real, c = kk - tap * c_real;
+      const int i = tap / g.k, j = tap - i * g.k;
+      off[kk] = (i * g.w + j) * g.c + c;
+    } else {
+      off[kk] = kk == Kr ? -1 : -2;
+    }
+  }
+  __syncthreads();
+  const bf16 one = __float2bfloat16_rn(1.f), zero = __float2bfloat16_rn(0.f);
+  const uint32_t total = (uint32_t)g.n * g.oh * g.ow * (uint32_t)(Kp / 8);
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    uint32_t m, ch, t, q, p, n;
+    d_chunks.divmod(e, m, ch);
+    d_ow.divmod(m, t, q);
+    d_oh.divmod(t, n, p);
+    const bf16* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
+    __align__(16) bf16 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int o = off[ch * 8 + u];
+      v[u] = o >= 0 ? base[o] : (o == -1 ? one : zero);
+    }
+    *(uint4*)(xcol + (size_t)m * Kp + ch * 8) = *(const uint4*)v;
+  }
+}
+
+// Wp[o][kk] = bf16(W[o][i][j][c]) for kk < Kr, 0 beyond (incl. the ones column)
+__global__ void pack_first_w_kernel(const float* __restrict__ w, int co, int k, int cp, int c_real, int Kp,
+                                    bf16* __restrict__ wp) {
+  const int Kr = k * k * c_real;
+  const size_t total = (size_t)co * Kp;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e / Kp), kk = (int)(e % Kp);
+    float v = 0.f;
+    if (kk < Kr) {
+      const int tap = kk / c_real, c = kk - tap * c_real;
+      v = w[((size_t)o * k * k + tap) * cp + c];
+    }
+    wp[e] = __float2bfloat16_rn(v);
+  }
+}
+
+inline int conv_fwd_packed(const ConvGeom& g, const bf16* xcol, int Kp, const bf16* wp, const float* bias, int relu,
+                           bf16* y, int num_sms, cudaStream_t st) {
+  const int M = g.n * g.oh * g.ow;
+  return with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.co, num_sms), [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(M, g.co, Kp, BN, 1);
+    DenseFwdLoader ld{};
+    ld.BN = BN;
+    if (!make_tmap_kmajor(&ld.amap, xcol, M, Kp, TC_BM) || !make_tmap_kmajor(&ld.bmap, wp, g.co, Kp, BN))
+      return fail(CE_ECUDA, "conv_fwd_packed: tensor map encoding failed");
+    FwdTcEpi ep{y, bias, M, g.co, relu};
+    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_packed: %s", cudaGetErrorString(e));
+  });
+}
+
+// A = xcol^T (MN-major over kk, 64x64 TMA boxes); B = dY (MN-major over C_out):
+// TMA boxes when C_out >= 64, else cp.async chunks gathered by the producers.
+template <bool TMA_B>
+struct WgradPackedLoader {
+  static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
+  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = TMA_B, PURE_TMA = TMA_B;
+  CUtensorMap amap;  // xcol [Mo][Kp]
+  CUtensorMap dmap;  // dY [Mo][co] (TMA_B)
+  const bf16* dy;
+  int co, Kp, Mo, BN;
+  __device__ void init(uint8_t*, int, int) const {}
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
+                       uint64_t* full) const {
+    if (ptid == 0) {
+      const int nblk = (c.m0 + 64 < Kp) ? 2 : 1;  // a fully out-of-range 64-row block is not loaded
+      mbar_expect_tx(full, (uint32_t)nblk * 64u * TC_BK * 2u + (TMA_B ? (uint32_t)BN * TC_BK * 2u : 0u));
+      for (int blk = 0; blk < nblk; ++blk) tma_load_2d(sA + blk * 8192, &amap, c.m0 + 64 * blk, kb * TC_BK, full);
+      if (TMA_B)
+        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &dmap, c.n0 + 64 * j, kb * TC_BK, full);
+    }
+    if (TMA_B) return;
+    const int groups = BN / 8;
+    for (int ch = ptid; ch < groups * TC_BK; ch += TC_PRODUCERS) {
+      const int grp = ch % groups, kr = ch / groups;
+      const int o0 = c.n0 + grp * 8, m = kb * TC_BK + kr;
+      const bool ok = o0 < co && m < Mo;
+      cp_async16(sB + mnmajor_off(BN, grp, kr), ok ? (const void*)(dy + (size_t)m * co + o0) : (const void*)dy,
+                 ok ? 16u : 0u);
+    }
+  }
+};
+
+inline int conv_wgrad_packed_splits(int Kp, int Mo, int num_sms) {
+  const int m_tiles = (Kp + TC_BM - 1) / TC_BM;
+  const long long nkb = ((long long)Mo + TC_BK - 1) / TC_BK;
+  long long want = num_sms / m_tiles;
+  if (want > nkb / 4) want = nkb / 4;
+  if (want > 128) want = 128;
+  return want < 1 ? 1 : (int)want;
+}
+
+// part[split][co][Kp]: split-K partial sums of D^T (row Kr = bias gradient)
+inline int conv_wgrad_packed(const ConvGeom& g, const bf16* xcol, int Kp, const bf16* dy, float* part,
+                             int* splits_out, int num_sms, cudaStream_t st) {
+  const int Mo = g.n * g.oh * g.ow;
+  return with_bn(g.co, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(Kp, g.co, Mo, BN, conv_wgrad_packed_splits(Kp, Mo, num_sms));
+    *splits_out = sh.splits;
+    WgradTcEpi ep{part, Kp, g.co};
+    cudaError_t e;
+    auto fill = [&](auto& ld) {
+      ld.dy = dy; ld.co = g.co; ld.Kp = Kp; ld.Mo = Mo; ld.BN = BN;
+    };
+    if constexpr (BN >= 64) {
+      WgradPackedLoader<true> ld{};
+      fill(ld);
+      if (!make_tmap_mn64(&ld.amap, xcol, Mo, Kp) || !make_tmap_mn64(&ld.dmap, dy, Mo, g.co))
+        return fail(CE_ECUDA, "conv_wgrad_packed: tensor map encoding failed");
+      e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    } else {
+      WgradPackedLoader<false> ld{};
+      fill(ld);
+      if (!make_tmap_mn64(&ld.amap, xcol, Mo, Kp)) return fail(CE_ECUDA, "conv_wgrad_packed: tensor map failed");
+      e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    }
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_wgrad_packed: %s", cudaGetErrorString(e));
+  });
+}
+
+// Reduce the split partials (one warp per element, fixed order) and apply the
+// momentum update (nn.py:306-322): kk < Kr -> master W[o][i][j][c] (+ packed
+// bf16 mirror), kk == Kr -> bias.
+__global__ void __launch_bounds__(256) conv_sgd_packed_kernel(
+    const float* __restrict__ part, int splits, int co, int Kp, int k, int cp, int c_real, float* __restrict__ w,
+    float* __restrict__ vel, float* __restrict__ gw, bf16* __restrict__ wp, float* __restrict__ b,
+    float* __restrict__ vb, float* __restrict__ gb, float lr, float mu) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int Kr = k * k * c_real;
+  const size_t e = (size_t)blockIdx.x * 8 + warp;  // over co x (Kr + 1)
+  if (e >= (size_t)co * (Kr + 1)) return;
+  const int o = (int)(e / (Kr + 1)), kk = (int)(e % (Kr + 1));
+  const float g = warp_sum_splits(part, splits, (size_t)co * Kp, (size_t)o * Kp + kk);
+  if (lane != 0) return;
+  if (kk == Kr) {
+    if (gb) gb[o] = g;
+    if (b) {
+      float bv = b[o], v = vb[o];
+      sgd_update(bv, v, g, lr, mu);
+      b[o] = bv;
+      vb[o] = v;
+    }
+    return;
+  }
+  const int tap = kk / c_real, c = kk - tap * c_real;
+  const size_t mi = ((size_t)o * k * k + tap) * cp + c;
+  if (gw) gw[mi] = g;
+  if (!w) return;
+  float wv = w[mi], vv = vel[mi];
+  sgd_update(wv, vv, g, lr, mu);
+  w[mi] = wv;
+  vel[mi] = vv;
+  if (wp) wp[(size_t)o * Kp + kk] = __float2bfloat16_rn(wv);
+}
+
+inline void launch_conv_sgd_packed(const float* part, int splits, const ConvGeom& g, int c_real, int Kp, float* w,
+                                   float* vel, float* gw, bf16* wp, float* b, float* vb, float* gb, float lr,
+                                   float mu, cudaStream_t st) {
+  const size_t elems = (size_t)g.co * (packed_kr(g, c_real) + 1);
+  conv_sgd_packed_kernel<<<(unsigned)((elems + 7) / 8), 256, 0, st>>>(part, splits, g.co, Kp, g.k, g.c, c_real, w,
+                                                                      vel, gw, wp, b, vb, gb, lr, mu);
+}
+
+inline void launch_im2col_packed(const bf16* x, const ConvGeom& g, int c_real, int Kp, bf16* xcol, cudaStream_t st) {
+  const size_t total = (size_t)g.n * g.oh * g.ow * (Kp / 8);
+  im2col_packed_kernel<<<grid_for(total), 256, 0, st>>>(x, g, c_real, Kp, FastDiv(Kp / 8), FastDiv(g.ow),
+                                                        FastDiv(g.oh), xcol);
+}
+
+}  // namespace ce

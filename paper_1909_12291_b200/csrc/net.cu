@@ -19,6 +19,7 @@
 #include "conv_tc.cuh"
 #include "dense_tc.cuh"
 #include "dense_simt.cuh"
+#include "first_layer_tc.cuh"
 #include "init.cuh"
 
 namespace ce {
@@ -51,6 +52,10 @@ struct Layer {
   int pidx = -1;
   float *W = nullptr, *b = nullptr, *VW = nullptr, *Vb = nullptr, *GW = nullptr, *Gb = nullptr;
   bf16 *Wbf = nullptr, *Wtbf = nullptr;
+  bool packed = false;    // conv over channel-padded input without dX: packed im2col GEMMs (first_layer_tc.cuh)
+  int Kp = 0;             // packed: im2col row width
+  bf16* Wp = nullptr;     // packed: bf16 mirror [co][Kp]
+  bf16* xcol = nullptr;   // packed: im2col matrix [B*oh*ow][Kp] of the last forward
   bf16* Wbp = nullptr;    // dense: bf16 mirror [out][in_pad]
   bf16* x16 = nullptr;    // dense after dense: bf16 copy of the fp32 input [B][in_pad]
   int in_pad = 0, out_pad = 0;
@@ -315,7 +320,12 @@ int enqueue_forward(ce_net* net, int n) {
       const double ab = (double)act_bytes(net);
       Prof pf(net, P_CONV_FWD, 2.0 * M * g.co * g.k * g.k * l.c_real,
               ab * ((double)n * g.h * g.w * g.c + (double)M * g.co + (double)g.co * K) + 4.0 * g.co);
-      if (net->use_tc) {
+      if (l.packed) {
+        launch_im2col_packed((const bf16*)in, g, l.c_real, l.Kp, l.xcol, st);
+        CE_CHECK_LAUNCH();
+        int s = conv_fwd_packed(g, l.xcol, l.Kp, l.Wp, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
+        if (s != CE_OK) return s;
+      } else if (net->use_tc) {
         int s = conv_fwd_tc(g, (const bf16*)in, l.Wbf, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
         if (s != CE_OK) return s;
       } else {
@@ -471,7 +481,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       int splits;
       {
       Prof pf(net, P_CONV_WGRAD, useful, ab * ((double)Mo * g.co + (double)n * g.h * g.w * g.c));
-      if (net->use_tc) {
+      if (l.packed) {
+        int s = conv_wgrad_packed(g, l.xcol, l.Kp, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
+        if (s != CE_OK) return s;
+        pf.bytes = ab * ((double)Mo * g.co + (double)Mo * l.Kp) + 4.0 * splits * g.co * l.Kp;
+      } else if (net->use_tc) {
         int s = conv_wgrad_tc(g, (const bf16*)x, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
         pf.bytes += 4.0 * splits * g.co * K;
@@ -483,6 +497,15 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
                   splits, st);
       }
       CE_CHECK_LAUNCH();
+      }
+      if (l.packed) {  // bias gradient = row Kr of the packed wgrad: no column-sum pass
+        Prof pf(net, P_CONV_SGD, 0.0, 4.0 * splits * g.co * l.Kp + 20.0 * g.co * (packed_kr(g, l.c_real) + 1));
+        launch_conv_sgd_packed(net->ws, splits, g, l.c_real, l.Kp, l.W, l.VW, keep ? l.GW : nullptr, l.Wp, l.b, l.Vb,
+                               keep ? l.Gb : nullptr, lr, mu, st);
+        CE_CHECK_LAUNCH();
+        if (!l.need_dx) break;
+        cur ^= 1;
+        continue;
       }
       float* bpart = net->ws + (size_t)splits * g.co * K;
       Prof pf(net, P_CONV_SGD, 0.0, ab * Mo * g.co + 4.0 * splits * g.co * K + 20.0 * g.co * K, 3);
@@ -797,6 +820,14 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         int sp = simt_splits((int)Mo, pick_splits(bps, Mo, 512, net->num_sms));
         sp = std::max(sp, conv_wgrad_tc_max_splits(l.g, (int)B, net->num_sms));
         ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);
+        l.packed = net->use_tc && l.c_real < l.g.c && !l.need_dx && !packed_disabled() &&
+                   packed_kp(l.g, l.c_real) <= kPackedMaxKp && Mo * packed_kp(l.g, l.c_real) / 8 < (1ll << 32);
+        if (l.packed) {
+          l.Kp = packed_kp(l.g, l.c_real);
+          const int psp = conv_wgrad_packed_splits(l.Kp, (int)Mo, net->num_sms);
+          ws = std::max(ws, (size_t)psp * l.g.co * l.Kp * 4);
+          ALLOC(l.xcol, (size_t)Mo * l.Kp * 2);
+        }
       }
     }
     if (l.wn) {
@@ -808,8 +839,12 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
       ALLOC(l.Vb, l.bn * 4);
 
       if (precision == CE_PREC_BF16 && l.kind == CE_LAYER_CONV) {
-        ALLOC(l.Wbf, l.wn * 2);
-        ALLOC(l.Wtbf, l.wn * 2);
+        if (l.packed) {
+          ALLOC(l.Wp, (size_t)l.g.co * l.Kp * 2);
+        } else {
+          ALLOC(l.Wbf, l.wn * 2);
+          ALLOC(l.Wtbf, l.wn * 2);
+        }
       }
       cudaMemsetAsync(l.W, 0, l.wn * 4, net->st);
       cudaMemsetAsync(l.VW, 0, l.wn * 4, net->st);
@@ -896,6 +931,9 @@ int ce_net_set_params(ce_net* net, int p, const float* w, const float* b) {
     f32_to_bf16_pad_kernel<<<grid_for((size_t)l.out_units * l.in_pad), 256, 0, st>>>(l.W, l.out_units, l.in_units,
                                                                                       l.in_pad, l.Wbp);
   if (l.Wtbf) conv_wt_kernel<<<grid_for(l.wn), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.s, l.g.c, l.Wtbf);
+  if (l.Wp)
+    pack_first_w_kernel<<<grid_for((size_t)l.g.co * l.Kp), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.c, l.c_real, l.Kp,
+                                                                         l.Wp);
   CE_CHECK_LAUNCH();
   CE_CUDA(cudaStreamSynchronize(st));
   return CE_OK;
@@ -938,6 +976,9 @@ int ce_net_init_uniform(ce_net* net, int p, uint64_t st_hi, uint64_t st_lo, uint
   if (l.Wbp)
     f32_to_bf16_pad_kernel<<<grid_for((size_t)l.out_units * l.in_pad), 256, 0, st>>>(l.W, l.out_units, l.in_units,
                                                                                       l.in_pad, l.Wbp);
+  if (l.Wp)
+    pack_first_w_kernel<<<grid_for((size_t)l.g.co * l.Kp), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.c, l.c_real, l.Kp,
+                                                                         l.Wp);
   CE_CHECK_LAUNCH();
   CE_CUDA(cudaStreamSynchronize(st));
   return CE_OK;

@@ -123,6 +123,14 @@ CE_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 CE_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Ties 16 tcgen05.ld destination registers to a point after tmem_ld_wait: their
+// consumers cannot be scheduled above this (volatile, ordered) statement.
+CE_DEV void tmem_regs_fence(uint32_t (&r)[16]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]));
+}
 
 // UMMA shared-memory descriptor, SWIZZLE_NONE ("interleaved") canonical layout.
 //   bits [0,14)  start address >> 4

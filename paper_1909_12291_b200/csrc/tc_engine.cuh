@@ -45,6 +45,15 @@ template <class Epi>
 struct EpiWarps<Epi, std::void_t<decltype(Epi::EPI_WARPS)>> {
   static constexpr int value = Epi::EPI_WARPS;
 };
+// Epilogues writing a row-major bf16 output may set STAGED_BF16: the engine then
+// converts 16 columns with epi.convert(), bounces the warp's 32 x 16 block
+// through shared memory and stores it two lanes per row (full 32-byte
+// sectors) instead of one 16-byte piece per row per lane.
+template <class Epi, class = void>
+struct EpiStaged : std::false_type {};
+template <class Epi>
+struct EpiStaged<Epi, std::void_t<decltype(Epi::STAGED_BF16)>> : std::bool_constant<Epi::STAGED_BF16> {};
+
 template <class Loader, class Epi>
 struct TcRoles {
   static constexpr int PW = ProducerWarps<Loader>::value;
@@ -105,7 +114,7 @@ __device__ inline TileCoord tc_tile(const TcShape& s, int t, int bn) {
   return c;
 }
 
-template <int BN>
+template <int BN, int EPI_STAGE = 0>
 struct TcSmemLayout {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
@@ -114,14 +123,15 @@ struct TcSmemLayout {
   static constexpr int LAG = STAGES - 1 > TC_MAX_LAG ? TC_MAX_LAG : STAGES - 1;  // cp.async groups in flight
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + TC_TABLE_BYTES + BAR_BYTES + 1024;  // + alignment slack
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + TC_TABLE_BYTES + BAR_BYTES + EPI_STAGE + 1024;  // + slack
 };
 
 template <int BN, class Loader, class Epi>
 __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Loader ld, const __grid_constant__ Epi epi, const TcShape shape) {
-  using L = TcSmemLayout<BN>;
   using R = TcRoles<Loader, Epi>;
+  constexpr bool STAGED = EpiStaged<Epi>::value;
+  using L = TcSmemLayout<BN, STAGED ? R::EW * 1024 : 0>;
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -131,6 +141,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base_slot = (uint32_t*)(tempty + 2);
+  uint8_t* epi_stage = table + TC_TABLE_BYTES + L::BAR_BYTES;  // STAGED: 1 KB per epilogue warp (16-B aligned)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -212,15 +223,55 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-      for (int col = col_begin; col < col_end; col += 16) {
-        uint32_t r[16];
-        tmem_ld16(tbase + col, r);
-        tmem_ld_wait();
-        float v[16];
+      if constexpr (STAGED) {
+        // software-pipelined: the TMEM load of the next chunk is in flight while this
+        // one is converted, staged (XOR-swizzled halves: conflict-free both ways) and
+        // stored; two named register sets, no runtime-indexed arrays
+        uint4* stage = (uint4*)(epi_stage + (warp - R::PW) * 1024);
+        auto emit = [&](int col, uint32_t (&r)[16]) {
+          float v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-        epi.store(c, row_in_tile, col, v);
+          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+          uint32_t out[8];
+          epi.convert(c, col, v, out);
+          const int sw = (lane >> 2) & 1;
+          stage[lane * 2 + sw] = make_uint4(out[0], out[1], out[2], out[3]);
+          stage[lane * 2 + (sw ^ 1)] = make_uint4(out[4], out[5], out[6], out[7]);
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 2; ++it) {
+            const int row = it * 16 + (lane >> 1), half = lane & 1;
+            bf16* dst = epi.row_ptr(c, q * 32 + row, col, half);
+            if (dst) *(uint4*)dst = stage[row * 2 + (half ^ ((row >> 2) & 1))];
+          }
+          __syncwarp();
+        };
+        uint32_t ra[16], rb[16];
+        if (col_begin < col_end) tmem_ld16(tbase + col_begin, ra);
+#pragma unroll 1
+        for (int col = col_begin; col < col_end; col += 32) {
+          tmem_ld_wait();
+          tmem_regs_fence(ra);
+          const bool more = col + 16 < col_end;
+          if (more) tmem_ld16(tbase + col + 16, rb);
+          emit(col, ra);
+          if (!more) break;
+          tmem_ld_wait();
+          tmem_regs_fence(rb);
+          if (col + 32 < col_end) tmem_ld16(tbase + col + 32, ra);
+          emit(col + 16, rb);
+        }
+      } else {
+#pragma unroll 1
+        for (int col = col_begin; col < col_end; col += 16) {
+          uint32_t r[16];
+          tmem_ld16(tbase + col, r);
+          tmem_ld_wait();
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+          epi.store(c, row_in_tile, col, v);
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -296,7 +347,7 @@ __device__ __forceinline__ uint32_t mnmajor_off(int R, int g, int kk) {
 
 template <int BN, class Loader, class Epi>
 inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& shape, int num_sms, cudaStream_t st) {
-  using L = TcSmemLayout<BN>;
+  using L = TcSmemLayout<BN, EpiStaged<Epi>::value ? TcRoles<Loader, Epi>::EW * 1024 : 0>;
   auto kern = tc_gemm_kernel<BN, Loader, Epi>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
   if (e != cudaSuccess) return e;
