@@ -20,6 +20,7 @@
 #include "dense_tc.cuh"
 #include "dense_simt.cuh"
 #include "first_layer_tc.cuh"
+#include "head.cuh"
 #include "init.cuh"
 
 namespace ce {
@@ -52,6 +53,7 @@ struct Layer {
   int pidx = -1;
   float *W = nullptr, *b = nullptr, *VW = nullptr, *Vb = nullptr, *GW = nullptr, *Gb = nullptr;
   bf16 *Wbf = nullptr, *Wtbf = nullptr;
+  bool head = false;      // final Dense with <= kHeadMaxOut outputs: fused forward+loss / backward (head.cuh)
   bool packed = false;    // conv over channel-padded input without dX: packed im2col GEMMs (first_layer_tc.cuh)
   int Kp = 0;             // packed: im2col row width
   bf16* Wp = nullptr;     // packed: bf16 mirror [co][Kp]
@@ -306,8 +308,12 @@ int pick_splits(long long blocks_per_split, long long K, long long min_chunk, in
 }
 
 // ----------------------------------------------------------------------------- forward
+// loss = true (training): a fused head also computes the loss and dL/dlogits
+// into gbuf[0] and sets *loss_fused.
 template <class T>
-int enqueue_forward(ce_net* net, int n) {
+int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nullptr) {
+  bool fused_dummy = false;
+  if (!loss_fused) loss_fused = &fused_dummy;
   cudaStream_t st = net->st;
   const void* in = net->x0;
   bool in_act = true;
@@ -341,6 +347,24 @@ int enqueue_forward(ce_net* net, int n) {
       CE_CHECK_LAUNCH();
     } else {
       const int B = n, K = l.in_units, O = l.out_units;
+      if (l.head) {  // logits (+ loss and dL/dlogits when training) in one kernel
+        const bool with_loss = loss && B <= kHeadMaxBatch;
+        Prof pf(net, P_DENSE_FWD, 2.0 * B * K * O, 4.0 * K * O + (in_act ? act_bytes(net) : 4.0) * B * K, 1);
+        unsigned* ticket = (unsigned*)(net->d_step + 2);
+        const int32_t* lab = with_loss ? net->ybatch : nullptr;
+        int s = in_act ? launch_head_fwd((const T*)in, K, l.W, l.b, B, K, O, net->ws, ticket, (float*)l.out, lab,
+                                         (float*)net->gbuf[0], net->d_losses, net->d_step, net->d_step + 1,
+                                         net->num_sms, st)
+                       : launch_head_fwd((const float*)in, K, l.W, l.b, B, K, O, net->ws, ticket, (float*)l.out, lab,
+                                         (float*)net->gbuf[0], net->d_losses, net->d_step, net->d_step + 1,
+                                         net->num_sms, st);
+        if (s != CE_OK) return s;
+        if (with_loss) *loss_fused = true;
+        CE_CHECK_LAUNCH();
+        in = l.out;
+        in_act = false;
+        continue;
+      }
       long long bps = simt_tiles(B, O);
       int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms, 8, 256));
       while (splits > 1 && (size_t)splits * B * O * 4 > net->ws_bytes) splits = simt_splits(K, splits - 1);
@@ -395,7 +419,21 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
     const void* gin = net->gbuf[cur];
     void* gout = net->gbuf[cur ^ 1];
     const T* mask = (l.mask_in && li > 0) ? (const T*)net->L[li - 1].out : nullptr;
-    if (l.kind == CE_LAYER_DENSE) {
+    if (l.kind == CE_LAYER_DENSE && l.head) {
+      const int B = n, K = l.in_units, O = l.out_units;
+      const float* g = (const float*)gin;
+      Prof pf(net, P_DENSE_BWD, (l.need_dx ? 4.0 : 2.0) * B * K * O,
+              20.0 * K * O + (l.need_dx ? 2.0 : 1.0) * (l.in_is_act ? act_bytes(net) : 4.0) * B * K, 1);
+      int s = l.in_is_act
+                  ? launch_head_bwd((const T*)x, K, g, B, K, O, l.W, l.VW, keep ? l.GW : nullptr,
+                                    l.need_dx ? (T*)gout : (T*)nullptr, mask, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu,
+                                    st)
+                  : launch_head_bwd((const float*)x, K, g, B, K, O, l.W, l.VW, keep ? l.GW : nullptr,
+                                    l.need_dx ? (float*)gout : (float*)nullptr, (const float*)nullptr, l.b, l.Vb,
+                                    keep ? l.Gb : nullptr, lr, mu, st);
+      if (s != CE_OK) return s;
+      CE_CHECK_LAUNCH();
+    } else if (l.kind == CE_LAYER_DENSE) {
       const int B = n, K = l.in_units, O = l.out_units;
       const float* g = (const float*)gin;
       Prof pf(net, P_DENSE_BWD, (l.need_dx ? 4.0 : 2.0) * B * K * O,
@@ -534,10 +572,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
 
 template <class T>
 int enqueue_step(ce_net* net, int n, float lr, float mu) {
-  int s = enqueue_forward<T>(net, n);
+  bool loss_fused = false;
+  int s = enqueue_forward<T>(net, n, true, &loss_fused);
   if (s != CE_OK) return s;
   const Layer& last = net->L.back();
-  {
+  if (!loss_fused) {
     Prof pf(net, P_LOSS, 0.0, 16.0 * n * net->classes);
     xent_kernel<int32_t><<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes,
                                           (float*)net->gbuf[0], net->d_losses, net->d_step, net->d_step + 1);
@@ -795,7 +834,10 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
       l.bn = l.out_units;
       l.in_pad = (l.in_units + 7) / 8 * 8;
       l.out_pad = (l.out_units + 7) / 8 * 8;
-      if (net->use_tc) {
+      l.head = i + 1 == net->L.size() && l.out_units <= kHeadMaxOut && !head_disabled();
+      if (l.head) {  // partial logits of the forward CTAs
+        ws = std::max(ws, (size_t)head_fwd_grid(l.in_units, net->num_sms, 1) * B * l.out_units * 4);
+      } else if (net->use_tc) {
         if (l.in_is_act && l.in_pad != l.in_units) return bail(fail(CE_EINVAL, "feature width not a multiple of 8"));
         ALLOC(l.Wbp, (size_t)l.out_units * l.in_pad * 2);
         if (!l.in_is_act) ALLOC(l.x16, B * (size_t)l.in_pad * 2);
@@ -860,7 +902,8 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
   ALLOC(net->ws, ws);
   net->ws_bytes = ws;
   if (gbf_elems) ALLOC(net->gbf, gbf_elems * 2);
-  ALLOC(net->d_step, 16);
+  ALLOC(net->d_step, 16);  // [0] step, [1] non-finite flag, [2] head ticket
+  cudaMemsetAsync(net->d_step, 0, 16, net->st);
   net->losses_cap = 4096;
   ALLOC(net->d_losses, net->losses_cap * 4);
   cudaError_t e = cudaStreamSynchronize(net->st);

@@ -189,9 +189,159 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(const TG* __restrict__
   }
 }
 
+// Strip forms: a thread walks kPoolStrip consecutive rows of one (pixel column,
+// 8-channel group) and keeps the window rows it still needs in registers, so
+// overlapping windows (S < K) load each input row once per thread instead of K
+// times. Same tie rule (first max in row-major window order) and the same
+// accumulation order (p, then q ascending) as the per-element kernels above.
+constexpr int kPoolStrip = 8;
+constexpr size_t kPoolStripMinWork = (size_t)148 * 2048 * 8;  // >= 8 strip rows per resident thread
+
+template <class T, int K, int S>
+__global__ void __launch_bounds__(256) maxpool_fwd_strip_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y,
+                                                                uint8_t* __restrict__ arg, bool relu_flag) {
+  const int cg = g.c / 8, strips = (g.oh + kPoolStrip - 1) / kPoolStrip;
+  const int total = g.n * strips * g.ow * cg;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int c0 = (e % cg) * 8;
+    int t = e / cg;
+    const int q = t % g.ow;
+    t /= g.ow;
+    const int sp = t % strips, n = t / strips;
+    const int p0 = sp * kPoolStrip, p1 = min(g.oh, p0 + kPoolStrip);
+    const T* col = x + ((size_t)n * g.h * g.w + (size_t)q * S) * g.c + c0;  // (row 0, col q*S)
+    float v[K][K][8];  // window rows i = 0..K-1 of the current output row
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j < K; ++j) load8(col + ((size_t)(p0 * S + i) * g.w + j) * g.c, v[i][j]);
+    for (int p = p0; p < p1; ++p) {
+      if (p > p0) {
+        if constexpr (S < K) {
+#pragma unroll
+          for (int i = 0; i < K - S; ++i)
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[i][j][u] = v[i + S][j][u];
+#pragma unroll
+          for (int i = K - S; i < K; ++i)
+#pragma unroll
+            for (int j = 0; j < K; ++j) load8(col + ((size_t)(p * S + i) * g.w + j) * g.c, v[i][j]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < K; ++i)
+#pragma unroll
+            for (int j = 0; j < K; ++j) load8(col + ((size_t)(p * S + i) * g.w + j) * g.c, v[i][j]);
+        }
+      }
+      float best[8];
+      uint8_t bi[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        best[u] = v[0][0][u];
+        bi[u] = 0;
+#pragma unroll
+        for (int tap = 1; tap < K * K; ++tap)
+          if (v[tap / K][tap % K][u] > best[u]) {
+            best[u] = v[tap / K][tap % K][u];
+            bi[u] = (uint8_t)tap;
+          }
+        if (relu_flag && !(best[u] > 0.f)) bi[u] = kPoolDead;
+      }
+      const size_t o = (((size_t)n * g.oh + p) * g.ow + q) * g.c + c0;
+      store8(y + o, best);
+      if (arg) *(uint2*)(arg + o) = *(const uint2*)bi;
+    }
+  }
+}
+
+// stride-1 backward: input row r receives from window rows p in [r-K+1, r]; the
+// thread keeps those K rows (dy + argmax of its K window columns) in a ring
+template <class T, class TG, int K>
+__global__ void __launch_bounds__(256) maxpool_bwd_s1_strip_kernel(const TG* __restrict__ dy,
+                                                                   const uint8_t* __restrict__ arg, ConvGeom g,
+                                                                   const T* __restrict__ mask, TG* __restrict__ dx) {
+  const int cg = g.c / 8, strips = (g.h + kPoolStrip - 1) / kPoolStrip;
+  const int total = g.n * strips * g.w * cg;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int c0 = (e % cg) * 8;
+    int t = e / cg;
+    const int xw = t % g.w;
+    t /= g.w;
+    const int sp = t % strips, n = t / strips;
+    const int r0 = sp * kPoolStrip, r1 = min(g.h, r0 + kPoolStrip);
+    // window columns q = xw - K + 1 + jj (jj = 0..K-1, ascending q)
+    float d[K][K][8];      // [ring row][jj][channel]
+    uint2 a[K][K];
+    bool ok[K][K];
+    auto load_row = [&](int slot, int p) {
+#pragma unroll
+      for (int jj = 0; jj < K; ++jj) {
+        const int qq = xw - K + 1 + jj;
+        ok[slot][jj] = p >= 0 && p < g.oh && qq >= 0 && qq < g.ow;
+        if (ok[slot][jj]) {
+          const size_t o = (((size_t)n * g.oh + p) * g.ow + qq) * g.c + c0;
+          a[slot][jj] = *(const uint2*)(arg + o);
+          load8(dy + o, d[slot][jj]);
+        }
+      }
+    };
+    // ring slot i holds window row p = r - K + 1 + i for the current input row r
+#pragma unroll
+    for (int i = 0; i < K; ++i) load_row(i, r0 - K + 1 + i);
+    for (int r = r0; r < r1; ++r) {
+      if (r > r0) {
+#pragma unroll
+        for (int i = 0; i < K - 1; ++i)
+#pragma unroll
+          for (int jj = 0; jj < K; ++jj) {
+            ok[i][jj] = ok[i + 1][jj];
+            a[i][jj] = a[i + 1][jj];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) d[i][jj][u] = d[i + 1][jj][u];
+          }
+        load_row(K - 1, r);
+      }
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < K; ++i)  // p ascending
+#pragma unroll
+        for (int jj = 0; jj < K; ++jj) {  // q ascending
+          if (!ok[i][jj]) continue;
+          // tap of (r, xw) inside window (p, q): (r - p) * K + (xw - q)
+          const uint8_t hit = (uint8_t)((K - 1 - i) * K + (K - 1 - jj));
+          const uint8_t* av = (const uint8_t*)&a[i][jj];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (av[u] == hit) acc[u] += d[i][jj][u];
+        }
+      const size_t off = (((size_t)n * g.h + r) * g.w + xw) * g.c + c0;
+      if (mask) {
+        float m[8];
+        load8(mask + off, m);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (!(m[u] > 0.f)) acc[u] = 0.f;
+      }
+      store8(dx + off, acc);
+    }
+  }
+}
+
 template <class T>
 int launch_maxpool_fwd(const T* x, const ConvGeom& g, T* y, uint8_t* arg, bool relu_flag, cudaStream_t st) {
-  const int grid = grid_for((size_t)g.n * g.oh * g.ow * (g.c / 8));
+  // strips only pay for overlapping windows on maps large enough to keep every SM busy
+  const size_t outs = (size_t)g.n * g.oh * g.ow * (g.c / 8);
+  if (g.s < g.k && outs >= kPoolStripMinWork) {
+    const int strips = (g.oh + kPoolStrip - 1) / kPoolStrip;
+    const int sgrid = grid_for((size_t)g.n * strips * g.ow * (g.c / 8));
+    if (g.k == 2) { maxpool_fwd_strip_kernel<T, 2, 1><<<sgrid, 256, 0, st>>>(x, g, y, arg, relu_flag); return CE_OK; }
+    if (g.s == 1) { maxpool_fwd_strip_kernel<T, 3, 1><<<sgrid, 256, 0, st>>>(x, g, y, arg, relu_flag); return CE_OK; }
+    maxpool_fwd_strip_kernel<T, 3, 2><<<sgrid, 256, 0, st>>>(x, g, y, arg, relu_flag);
+    return CE_OK;
+  }
+  const int grid = grid_for(outs);
 #define CE_POOL_F(KK, SS) \
   if (g.k == KK && g.s == SS) { maxpool_fwd_kernel<T, KK, SS><<<grid, 256, 0, st>>>(x, g, y, arg, relu_flag); return CE_OK; }
   CE_POOL_F(2, 1) CE_POOL_F(2, 2) CE_POOL_F(2, 3) CE_POOL_F(3, 1) CE_POOL_F(3, 2) CE_POOL_F(3, 3)
@@ -201,6 +351,12 @@ int launch_maxpool_fwd(const T* x, const ConvGeom& g, T* y, uint8_t* arg, bool r
 
 template <class T, class TG>
 int launch_maxpool_bwd(const TG* dy, const uint8_t* arg, const ConvGeom& g, const T* mask, TG* dx, cudaStream_t st) {
+  if (g.s == 1 && (size_t)g.n * g.h * g.w * (g.c / 8) >= kPoolStripMinWork) {
+    const int strips = (g.h + kPoolStrip - 1) / kPoolStrip;
+    const int sgrid = grid_for((size_t)g.n * strips * g.w * (g.c / 8));
+    if (g.k == 2) { maxpool_bwd_s1_strip_kernel<T, TG, 2><<<sgrid, 256, 0, st>>>(dy, arg, g, mask, dx); return CE_OK; }
+    if (g.k == 3) { maxpool_bwd_s1_strip_kernel<T, TG, 3><<<sgrid, 256, 0, st>>>(dy, arg, g, mask, dx); return CE_OK; }
+  }
   const int grid = grid_for((size_t)g.n * g.h * g.w * (g.c / 8));
 #define CE_POOL_B(KK, SS) \
   if (g.k == KK && g.s == SS) { maxpool_bwd_kernel<T, TG, KK, SS><<<grid, 256, 0, st>>>(dy, arg, g, mask, dx); return CE_OK; }

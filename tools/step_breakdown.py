@@ -8,7 +8,7 @@ rows = list(csv.reader(open(sys.argv[1])))
 hdr = [r for r in rows if "Kernel Name" in r][0]
 k, v, g = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Grid Size")
 seq = [(r[k], float(r[v].replace(",", "")) / 1e3, r[g]) for r in rows if len(r) == len(hdr) and r is not hdr]
-xs = [i for i, (n, _, _) in enumerate(seq) if "xent_kernel" in n]
+xs = [i for i, (n, _, _) in enumerate(seq) if "xent_kernel" in n or "head_fwd_kernel" in n]
 a, b = xs[1], xs[2]
 tot = 0.0
 for n, t, grid in seq[a - 30 if a > 30 else 0:b + 1][:0] or seq[xs[1] + 1: xs[2] + 1]:
