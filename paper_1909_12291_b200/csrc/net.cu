@@ -1371,8 +1371,12 @@ int ce_latency(ce_net* net, const float* x, int n, int warmup, int reps, double*
   DevGuard dg(net->device);
   // exclusive per-GPU window: no other slot enqueues while we hold the gate, and
   // what they already enqueued drains before the first timed forward
-  ExclusiveGate gate(net->device);
-  CE_CUDA(cudaDeviceSynchronize());
+  static const bool shared_window = [] {  // CE_LATENCY_SHARED=1: no exclusive window (comparison only)
+    const char* e = getenv("CE_LATENCY_SHARED");
+    return e && e[0] == '1';
+  }();
+  ExclusiveGate gate(shared_window ? -1 : net->device);
+  if (!shared_window) CE_CUDA(cudaDeviceSynchronize());
   cudaStream_t st = net->st;
   net->acc = 0;
   if (int s = upload_host_batch(net, x, n)) return s;

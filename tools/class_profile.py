@@ -1,6 +1,7 @@
 """Per-genome kernel-class profile of the C2 population (library per-class CUDA
 events, steps run un-graphed): ms and launches per class per genome.
-    python tools/class_profile.py [precision]
+    python tools/class_profile.py [precision] [max_batches_per_epoch]
+(a small max_batches_per_epoch keeps ncu launch-list passes short)
 """
 import sys
 
@@ -10,13 +11,14 @@ from paper_1909_12291_b200 import (EvolutionSettings, Master, ObjectiveConfig, S
 from paper_1909_12291_b200.patches import default_splits
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "bf16"
+mbe = int(sys.argv[2]) if len(sys.argv) > 2 else None
 splits = default_splits()
 m = Master(SearchSpace(), ObjectiveConfig("flop_proxy", -0.2, 1.0, 2.0), EvolutionSettings(capacity=16, max_evaluations=16), seed=0)
 pop = [m.issue("w") for _ in range(16)]
 obj = ObjectiveConfig("measured_latency", -0.2, 1e-5, 1e-2)
 tot = {}
 for i, g in enumerate(pop):
-    r = evaluate(g, splits, TrainBudget(), obj, seed=0, precision=prec, profile=True)
+    r = evaluate(g, splits, TrainBudget(max_batches_per_epoch=mbe), obj, seed=0, precision=prec, profile=True)
     prof = r.extras.get("kernel_profile", {})
     steps = r.extras.get("train_steps", 0)
     parts = []
