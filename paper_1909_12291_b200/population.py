@@ -7,7 +7,7 @@ comes back to the host, nothing else does (no collective).
 
 import numpy as np
 
-from .candidate import TrainBudget, evaluate
+from .candidate import LatencyWindow, TrainBudget, evaluate
 from .genes import validate_shapes
 from .scheduler import GpuPool
 
@@ -64,19 +64,26 @@ class ListMaster:
 
 
 def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), slots_per_gpu=2,
-                        order="lpt", precision="bf16", **evaluate_kwargs):
-    """Evaluate every genome; returns (records in input order, PoolReport)."""
+                        order="lpt", precision="bf16", defer_latency=True, **evaluate_kwargs):
+    """Evaluate every genome; returns (records in input order, PoolReport).
+
+    The generation is pre-issued, so with defer_latency the measured-latency
+    objectives are taken in one exclusive pass once every slot is done
+    (candidate.LatencyWindow) instead of stalling the other slots per candidate."""
     master = ListMaster(genomes)
     n_train = len(splits.train)
+    window = LatencyWindow() if defer_latency else None
 
     def run_one(genome, worker_id, device):
         return evaluate(genome, splits, budget, objective, seed, worker_id=worker_id,
-                        precision=precision, device=device, **evaluate_kwargs)
+                        precision=precision, device=device, latency_window=window, **evaluate_kwargs)
 
     pool = GpuPool(run_one, master, devices=devices, slots_per_gpu=slots_per_gpu, order=order,
                    cost_fn=lambda g: estimate_cost(g, n_train, budget))
     report = pool.run()
     report.trace = pool.trace
+    if window is not None:
+        window.flush()
     return [master.records.get(g.id) for g in master.genomes], report
 
 
