@@ -196,6 +196,173 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// Split-K dense forward on CUDA cores (fp32 check mode, small batch):
+// part[split][b][o] = sum over the split's k-range of x[b][k] W[o][k].
+// Block = 256 outputs x 32 rows, 256 threads: lane -> 8 outputs (o = lane + 32 j),
+// warp -> 4 rows. W is staged [o][k] with a 33-float stride (conflict-free fill
+// from float4 rows and conflict-free per-lane reads), x is staged [k][b] and
+// read as warp-uniform float4 broadcasts; the next K chunk is fetched into
+// registers while the current one is consumed (one barrier per chunk).
+constexpr int DF_TB = 32, DF_KC = 32, DF_WS = DF_KC + 4, DF_XS = DF_TB + 4;
+template <int R>
+constexpr int df_smem() { return 2 * (32 * R * DF_WS + DF_KC * DF_XS) * 4; }
+// R outputs per lane: block tile 32R outputs (R chosen per layer to limit padding)
+template <class TX, int R>
+__global__ void __launch_bounds__(256, 2) dense_fwd_simt_kernel(const TX* __restrict__ x, const float* __restrict__ w,
+                                                                int B, int in, int out, int kchunk,
+                                                                float* __restrict__ part) {
+  constexpr int DF_TO = 32 * R;
+  extern __shared__ __align__(16) float dsm[];
+  // buffer b: W at dsm + b * DF_TO * DF_WS, x at xs0 + b * DF_KC * DF_XS
+  float* const xs0 = dsm + 2 * DF_TO * DF_WS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ob = blockIdx.x * DF_TO, bb = blockIdx.y * DF_TB;
+  const int k0 = blockIdx.z * kchunk, k1 = min(in, k0 + kchunk);
+  const bool kvec = (in & 3) == 0;
+  // fetch mapping: W: 8 float4 per thread (row = tid/8 + 32 i, kq = tid % 8); x: 1 float4 (b = tid/8)
+  const int frow = tid >> 3, fkq = tid & 7;
+  float4 rw[R], rx;
+  auto fetch = [&](int kc) {
+    const int k = kc + fkq * 4;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int o = ob + frow + 32 * i;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (o < out) {
+        const float* src = w + (size_t)o * in;
+        if (kvec && k + 3 < k1) {
+          v = *(const float4*)(src + k);
+        } else {
+          v.x = k < k1 ? src[k] : 0.f;
+          v.y = k + 1 < k1 ? src[k + 1] : 0.f;
+          v.z = k + 2 < k1 ? src[k + 2] : 0.f;
+          v.w = k + 3 < k1 ? src[k + 3] : 0.f;
+        }
+      }
+      rw[i] = v;
+    }
+    const int b = bb + frow;
+    rx = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (b < B) {
+      const TX* src = x + (size_t)b * in;
+      rx.x = k < k1 ? ldf(src, k) : 0.f;
+      rx.y = k + 1 < k1 ? ldf(src, k + 1) : 0.f;
+      rx.z = k + 2 < k1 ? ldf(src, k + 2) : 0.f;
+      rx.w = k + 3 < k1 ? ldf(src, k + 3) : 0.f;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      *(float4*)(dsm + buf * (DF_TO * DF_WS) + (frow + 32 * i) * DF_WS + fkq * 4) = rw[i];
+    float* d = xs0 + buf * (DF_KC * DF_XS) + (fkq * 4) * DF_XS + frow;
+    d[0] = rx.x; d[DF_XS] = rx.y; d[2 * DF_XS] = rx.z; d[3 * DF_XS] = rx.w;
+  };
+  float acc[R][4];
+#pragma unroll
+  for (int j = 0; j < R; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  if (k0 < k1) {
+    fetch(k0);
+    stash(0);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int kc = k0; kc < k1; kc += DF_KC) {
+    const bool more = kc + DF_KC < k1;
+    if (more) fetch(kc + DF_KC);
+    const float* W = dsm + buf * (DF_TO * DF_WS);
+    const float* X = xs0 + buf * (DF_KC * DF_XS);
+#pragma unroll 2
+    for (int kk = 0; kk < DF_KC; kk += 4) {
+      // W rows (stride 36 floats: the 8 lanes of a phase hit distinct bank quads)
+      float4 wq[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) wq[j] = *(const float4*)(W + (lane + 32 * j) * DF_WS + kk);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 xv = *(const float4*)(X + (kk + u) * DF_XS + warp * 4);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const float wv = u == 0 ? wq[j].x : u == 1 ? wq[j].y : u == 2 ? wq[j].z : wq[j].w;
+          acc[j][0] = fmaf(xv.x, wv, acc[j][0]);
+          acc[j][1] = fmaf(xv.y, wv, acc[j][1]);
+          acc[j][2] = fmaf(xv.z, wv, acc[j][2]);
+          acc[j][3] = fmaf(xv.w, wv, acc[j][3]);
+        }
+      }
+    }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  float* dst = part + (size_t)blockIdx.z * B * out;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int b = bb + warp * 4 + r;
+    if (b >= B) break;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int o = ob + lane + 32 * j;
+      if (o < out) dst[(size_t)b * out + o] = acc[j][r];
+    }
+  }
+}
+
+// CE_DENSE_FWD_GEMM=1 keeps the generic SIMT GEMM for the fp32 dense forward (comparison)
+inline bool dense_fwd_simt_enabled() {
+  static const bool off = [] {
+    const char* e = getenv("CE_DENSE_FWD_GEMM");
+    return e && e[0] == '1';
+  }();
+  return !off;
+}
+
+// outputs per lane minimising padded outputs (ties -> larger tiles)
+inline int dense_fwd_simt_r(int out) {
+  int best = 8;
+  long long best_pad = -1;
+  for (int r : {8, 6, 4}) {
+    const long long pad = (long long)((out + 32 * r - 1) / (32 * r)) * 32 * r;
+    if (best_pad < 0 || pad < best_pad) best_pad = pad, best = r;
+  }
+  return best;
+}
+
+inline int dense_fwd_simt_splits(int B, int in, int out, int num_sms) {
+  const int to = 32 * dense_fwd_simt_r(out);
+  const long long blocks = (long long)((out + to - 1) / to) * ((B + DF_TB - 1) / DF_TB);
+  long long s = (2LL * num_sms + blocks - 1) / blocks;
+  const long long cap = (in + 255) / 256;
+  if (s > cap) s = cap;
+  if (s > 256) s = 256;
+  return s < 1 ? 1 : (int)s;
+}
+
+template <class TX, int R>
+inline int dense_fwd_simt_r_launch(const TX* x, const float* w, int B, int in, int out, int splits, float* part,
+                                   cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dense_fwd_simt_kernel<TX, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, df_smem<R>());
+    attr = true;
+  }
+  const int kchunk = ((in + splits - 1) / splits + DF_KC - 1) / DF_KC * DF_KC;
+  const int s = (in + kchunk - 1) / kchunk;
+  dim3 grid((out + 32 * R - 1) / (32 * R), (B + DF_TB - 1) / DF_TB, s);
+  dense_fwd_simt_kernel<TX, R><<<grid, 256, df_smem<R>(), st>>>(x, w, B, in, out, kchunk, part);
+  return s;
+}
+
+template <class TX>
+inline int dense_fwd_simt(const TX* x, const float* w, int B, int in, int out, int splits, float* part,
+                          cudaStream_t st) {
+  switch (dense_fwd_simt_r(out)) {
+    case 4: return dense_fwd_simt_r_launch<TX, 4>(x, w, B, in, out, splits, part, st);
+    case 6: return dense_fwd_simt_r_launch<TX, 6>(x, w, B, in, out, splits, part, st);
+    default: return dense_fwd_simt_r_launch<TX, 8>(x, w, B, in, out, splits, part, st);
+  }
+}
+
 // fp32 check mode: these kernels up to B = 64, the generic SIMT GEMM above.
 constexpr int kDenseSimtMaxBatch = 64;
 // bf16: measured on B200 (C2 heads, 51-137 M params): the FFMA dW+SGD pass

@@ -379,6 +379,11 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
         }
         int s = dense_fwd_tc(x16, l.in_pad, l.Wbp, K, l.in_pad, O, B, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
+      } else if (dense_fwd_simt_enabled()) {
+        splits = dense_fwd_simt_splits(B, K, O, net->num_sms);
+        while (splits > 1 && (size_t)splits * B * O * 4 > net->ws_bytes) --splits;
+        splits = in_act ? dense_fwd_simt((const T*)in, l.W, B, K, O, splits, net->ws, st)
+                        : dense_fwd_simt((const float*)in, l.W, B, K, O, splits, net->ws, st);
       } else {
         PartialEpi pe{net->ws, B, O};
         if (in_act)
@@ -848,6 +853,8 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
       long long bps = simt_tiles((int)B, l.out_units);
       int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms, 8, 256));
       ws = std::max(ws, (size_t)sp * B * l.out_units * 4);
+      ws = std::max(ws, (size_t)dense_fwd_simt_splits((int)B, l.in_units, l.out_units, net->num_sms) * B *
+                            l.out_units * 4);
       ws = std::max(ws, (size_t)(kColsumMaxSplits + 64) * l.out_units * 4);
     } else {
       ALLOC(l.out, B * l.out_per_sample * ab);
