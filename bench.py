@@ -23,6 +23,7 @@ numpy oracle port (oracle/cnn_ref.py) on a bounded sample on this host.
 """
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -49,6 +50,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--slots", type=int, default=4, help="candidates packed per GPU (streams)")
+    ap.add_argument("--order", choices=["lpt", "two_ended", "fifo"], default="two_ended",
+                    help="dispatch order of the pre-issued population")
     ap.add_argument("--precision", choices=["bf16", "fp32"], default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -249,12 +252,14 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     last_trace = []
+    last_window = [0.0]
 
     def step(profile=False):
         recs, report = evaluate_population(mine, splits, budget, obj, seed=0, devices=(device,),
                                            slots_per_gpu=1 if profile else args.slots, precision=args.precision,
-                                           profile=profile)
+                                           profile=profile, order=args.order)
         last_trace[:] = getattr(report, "trace", [])
+        last_window[0] = getattr(report, "latency_window_s", 0.0)
         return recs
 
     def timed(n_steps, e2e=False):
@@ -281,7 +286,12 @@ def main():
         step()
     clocks = ClockSampler(device)
     clocks.start()
-    times, launches, recs = timed(args.steps)
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed steps (host objects are few and short-lived)
+    try:
+        times, launches, recs = timed(args.steps)
+    finally:
+        gc.enable()
     clock_info = clocks.stop()
     if os.environ.get("BENCH_TRACE"):  # per-candidate timeline of the last timed step (stderr)
         t0 = min(t[2] for t in last_trace)
@@ -289,6 +299,7 @@ def main():
         for gid, wid, a, b in sorted(last_trace, key=lambda t: t[2]):
             print(f"trace {wid} g{idx.get(gid, -1):02d} start {1000 * (a - t0):8.1f} ms  dur {1000 * (b - a):8.1f} ms",
                   file=sys.stderr)
+        print(f"trace latency window {1000 * last_window[0]:.1f} ms", file=sys.stderr)
     ms = allreduce([statistics.fmean(times)])[0]
     launches = int(allreduce([launches], "sum")[0])
     total_candidates = POP_PER_GPU * world

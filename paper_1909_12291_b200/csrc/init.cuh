@@ -70,7 +70,10 @@ __device__ __forceinline__ size_t init_dev_index(const InitLayout& L, size_t r) 
   return r;
 }
 
-constexpr int kInitChunk = 2048;
+// draws per thread: each is one link of a dependent 128-bit LCG chain, so the chunk
+// length bounds the kernel latency; the per-thread jump-ahead (~2 log2(n) u128
+// multiply-adds) is amortised over it
+constexpr int kInitChunk = 128;
 
 // numpy Generator.uniform(lo, lo + range): lo + range * next_double, in double,
 // then cast to float32 (the .astype of nn.py:46). Draw r of the stream (after

@@ -1030,7 +1030,8 @@ int ce_net_init_uniform(ce_net* net, int p, uint64_t st_hi, uint64_t st_lo, uint
     pack_first_w_kernel<<<grid_for((size_t)l.g.co * l.Kp), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.c, l.c_real, l.Kp,
                                                                          l.Wp);
   CE_CHECK_LAUNCH();
-  CE_CUDA(cudaStreamSynchronize(st));
+  // no host buffers involved: the draws stay stream-ordered before the net's next
+  // work (training / forward on the same stream), so no synchronisation here
   return CE_OK;
 }
 

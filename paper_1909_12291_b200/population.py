@@ -5,6 +5,8 @@ the GA host (ga.Master) or a fixed genome list feeds a GpuPool; each record
 comes back to the host, nothing else does (no collective).
 """
 
+import time
+
 import numpy as np
 
 from .candidate import LatencyWindow, TrainBudget, evaluate
@@ -64,8 +66,13 @@ class ListMaster:
 
 
 def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), slots_per_gpu=2,
-                        order="lpt", precision="bf16", defer_latency=True, **evaluate_kwargs):
+                        order="two_ended", precision="bf16", defer_latency=True, **evaluate_kwargs):
     """Evaluate every genome; returns (records in input order, PoolReport).
+
+    order "two_ended" (default): slot 0 of each GPU takes the longest remaining
+    candidate, the other slots the shortest, so heavy candidates (whose kernels
+    fill the GPU alone) mostly run one at a time beside light, latency-bound
+    ones; measured on C2 it is faster and steadier than plain LPT ("lpt").
 
     The generation is pre-issued, so with defer_latency the measured-latency
     objectives are taken in one exclusive pass once every slot is done
@@ -83,7 +90,9 @@ def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), 
     report = pool.run()
     report.trace = pool.trace
     if window is not None:
+        t0 = time.perf_counter()
         window.flush()
+        report.latency_window_s = time.perf_counter() - t0
     return [master.records.get(g.id) for g in master.genomes], report
 
 
