@@ -196,6 +196,94 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// Same dX tile with the next 32-output chunk of W / G fetched into registers while
+// the current one is consumed (double-buffered shared memory, one barrier per
+// chunk); used when in % 4 == 0 (float4 rows of W).
+constexpr int DXP_SMEM = 2 * (DS_KC * DS_TI + DS_KC * DS_TR) * 4;
+template <class TO, class TM>
+__global__ void __launch_bounds__(256, 2)
+    dense_dx_simt_pipe_kernel(const float* __restrict__ g, const float* __restrict__ w, int B, int in, int out,
+                              const TM* __restrict__ mask, TO* __restrict__ dx) {
+  extern __shared__ __align__(16) float dxs[];
+  float* const gs0 = dxs + 2 * DS_KC * DS_TI;
+  const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
+  const int bb0 = blockIdx.x * DS_TR, ib = blockIdx.y * DS_TI;
+  const int i0 = ib + tx * 4, b0 = bb0 + ty * 8;
+  float4 rw[8];
+  float rg[4];
+  auto fetch = [&](int oc) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // e = tid + 256 j -> (oo = e / 64, q = e % 64)
+      const int e = tid + 256 * j, oo = e >> 6, q = e & 63, i = ib + q * 4;
+      rw[j] = (oc + oo < out && i < in) ? *(const float4*)(w + (size_t)(oc + oo) * in + i)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // e = tid + 256 j -> (oo = e / 32, bl = e % 32)
+      const int e = tid + 256 * j, oo = e >> 5, bl = e & 31, b = bb0 + bl;
+      rg[j] = (oc + oo < out && b < B) ? g[(size_t)b * out + oc + oo] : 0.f;
+    }
+  };
+  auto stash = [&](int buf) {
+    float* W = dxs + buf * (DS_KC * DS_TI);
+    float* G = gs0 + buf * (DS_KC * DS_TR);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = tid + 256 * j;
+      *(float4*)(W + (e >> 6) * DS_TI + (e & 63) * 4) = rw[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = tid + 256 * j;
+      G[(e >> 5) * DS_TR + (e & 31)] = rg[j];
+    }
+  };
+  float acc[8][4];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int oc = 0; oc < out; oc += DS_KC) {
+    const bool more = oc + DS_KC < out;
+    if (more) fetch(oc + DS_KC);
+    const float* W = dxs + buf * (DS_KC * DS_TI);
+    const float* G = gs0 + buf * (DS_KC * DS_TR);
+    const int n = min(DS_KC, out - oc);
+#pragma unroll 4
+    for (int oo = 0; oo < n; ++oo) {
+      const float4 wv = *(const float4*)(W + oo * DS_TI + tx * 4);
+      const float4 ga = *(const float4*)(G + oo * DS_TR + ty * 8), gb = *(const float4*)(G + oo * DS_TR + ty * 8 + 4);
+      const float g8[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+      fma8x4(acc, g8, wv);
+    }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int b = b0 + r;
+    if (b >= B) continue;
+    const size_t off = (size_t)b * in + i0;
+    if (i0 + 3 < in) {
+      float v[4] = {acc[r][0], acc[r][1], acc[r][2], acc[r][3]};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (mask && !(ldf(mask, off + j) > 0.f)) v[j] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) stf(dx, off + j, v[j]);
+    } else {
+      for (int j = 0; j < 4 && i0 + j < in; ++j) {
+        float v = acc[r][j];
+        if (mask && !(ldf(mask, off + j) > 0.f)) v = 0.f;
+        stf(dx, off + j, v);
+      }
+    }
+  }
+}
+
 // Split-K dense forward on CUDA cores (fp32 check mode, small batch):
 // part[split][b][o] = sum over the split's k-range of x[b][k] W[o][k].
 // Block = 256 outputs x 32 rows, 256 threads: lane -> 8 outputs (o = lane + 32 j),
@@ -341,11 +429,7 @@ inline int dense_fwd_simt_splits(int B, int in, int out, int num_sms) {
 template <class TX, int R>
 inline int dense_fwd_simt_r_launch(const TX* x, const float* w, int B, int in, int out, int splits, float* part,
                                    cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dense_fwd_simt_kernel<TX, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, df_smem<R>());
-    attr = true;
-  }
+  cudaFuncSetAttribute(dense_fwd_simt_kernel<TX, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, df_smem<R>());
   const int kchunk = ((in + splits - 1) / splits + DF_KC - 1) / DF_KC * DF_KC;
   const int s = (in + kchunk - 1) / kchunk;
   dim3 grid((out + 32 * R - 1) / (32 * R), (B + DF_TB - 1) / DF_TB, s);
@@ -404,6 +488,12 @@ template <class TO, class TM>
 inline void dense_dx_simt(const float* g, const float* w, int B, int in, int out, const TM* mask, TO* dx,
                           cudaStream_t st) {
   dim3 grid(cdiv(B, DS_TR), cdiv(in, DS_TI));
+  if ((in & 3) == 0) {
+    // per device (a process may drive several GPUs): set on every launch, it is cheap
+    cudaFuncSetAttribute(dense_dx_simt_pipe_kernel<TO, TM>, cudaFuncAttributeMaxDynamicSharedMemorySize, DXP_SMEM);
+    dense_dx_simt_pipe_kernel<TO, TM><<<grid, 256, DXP_SMEM, st>>>(g, w, B, in, out, mask, dx);
+    return;
+  }
   dense_dx_simt_kernel<TO, TM><<<grid, 256, 0, st>>>(g, w, B, in, out, mask, dx);
 }
 
