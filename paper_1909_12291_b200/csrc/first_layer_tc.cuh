@@ -37,9 +37,10 @@ inline int packed_kp(const ConvGeom& g, int c_real) { return (packed_kr(g, c_rea
 // block in shared memory (-1: the ones column, -2: zero padding); index math
 // is 32-bit with magic-number division.
 constexpr int kPackedMaxKp = 1024;
-__global__ void __launch_bounds__(256) im2col_packed_kernel(const bf16* __restrict__ x, ConvGeom g, int c_real,
+template <class T>
+__global__ void __launch_bounds__(256) im2col_packed_kernel(const T* __restrict__ x, ConvGeom g, int c_real,
                                                             int Kp, FastDiv d_chunks, FastDiv d_ow, FastDiv d_oh,
-                                                            bf16* __restrict__ xcol) {
+                                                            T* __restrict__ xcol) {
   __shared__ int off[kPackedMaxKp];
   const int Kr = g.k * g.k * c_real;
   for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
@@ -52,27 +53,27 @@ __global__ void __launch_bounds__(256) im2col_packed_kernel(const bf16* __restri
     }
   }
   __syncthreads();
-  const bf16 one = __float2bfloat16_rn(1.f), zero = __float2bfloat16_rn(0.f);
   const uint32_t total = (uint32_t)g.n * g.oh * g.ow * (uint32_t)(Kp / 8);
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     uint32_t m, ch, t, q, p, n;
     d_chunks.divmod(e, m, ch);
     d_ow.divmod(m, t, q);
     d_oh.divmod(t, n, p);
-    const bf16* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
-    __align__(16) bf16 v[8];
+    const T* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
+    float v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int o = off[ch * 8 + u];
-      v[u] = o >= 0 ? base[o] : (o == -1 ? one : zero);
+      v[u] = o >= 0 ? ldf(base, (size_t)o) : (o == -1 ? 1.f : 0.f);
     }
-    *(uint4*)(xcol + (size_t)m * Kp + ch * 8) = *(const uint4*)v;
+    store8(xcol + (size_t)m * Kp + ch * 8, v);  // bf16 values round-trip exactly
   }
 }
 
 // Wp[o][kk] = bf16(W[o][i][j][c]) for kk < Kr, 0 beyond (incl. the ones column)
+template <class TW>
 __global__ void pack_first_w_kernel(const float* __restrict__ w, int co, int k, int cp, int c_real, int Kp,
-                                    bf16* __restrict__ wp) {
+                                    TW* __restrict__ wp) {
   const int Kr = k * k * c_real;
   const size_t total = (size_t)co * Kp;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
@@ -82,7 +83,7 @@ __global__ void pack_first_w_kernel(const float* __restrict__ w, int co, int k, 
       const int tap = kk / c_real, c = kk - tap * c_real;
       v = w[((size_t)o * k * k + tap) * cp + c];
     }
-    wp[e] = __float2bfloat16_rn(v);
+    stf(wp, e, v);
   }
 }
 
@@ -175,9 +176,10 @@ inline int conv_wgrad_packed(const ConvGeom& g, const bf16* xcol, int Kp, const 
 // Reduce the split partials (one warp per element, fixed order) and apply the
 // momentum update (nn.py:306-322): kk < Kr -> master W[o][i][j][c] (+ packed
 // bf16 mirror), kk == Kr -> bias.
+template <class TW>
 __global__ void __launch_bounds__(256) conv_sgd_packed_kernel(
     const float* __restrict__ part, int splits, int co, int Kp, int k, int cp, int c_real, float* __restrict__ w,
-    float* __restrict__ vel, float* __restrict__ gw, bf16* __restrict__ wp, float* __restrict__ b,
+    float* __restrict__ vel, float* __restrict__ gw, TW* __restrict__ wp, float* __restrict__ b,
     float* __restrict__ vb, float* __restrict__ gb, float lr, float mu) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Kr = k * k * c_real;
@@ -204,21 +206,35 @@ __global__ void __launch_bounds__(256) conv_sgd_packed_kernel(
   sgd_update(wv, vv, g, lr, mu);
   w[mi] = wv;
   vel[mi] = vv;
-  if (wp) wp[(size_t)o * Kp + kk] = __float2bfloat16_rn(wv);
+  if (wp) stf(wp, (size_t)o * Kp + kk, wv);
 }
 
+template <class TW>
 inline void launch_conv_sgd_packed(const float* part, int splits, const ConvGeom& g, int c_real, int Kp, float* w,
-                                   float* vel, float* gw, bf16* wp, float* b, float* vb, float* gb, float lr,
+                                   float* vel, float* gw, TW* wp, float* b, float* vb, float* gb, float lr,
                                    float mu, cudaStream_t st) {
   const size_t elems = (size_t)g.co * (packed_kr(g, c_real) + 1);
-  conv_sgd_packed_kernel<<<(unsigned)((elems + 7) / 8), 256, 0, st>>>(part, splits, g.co, Kp, g.k, g.c, c_real, w,
-                                                                      vel, gw, wp, b, vb, gb, lr, mu);
+  conv_sgd_packed_kernel<TW><<<(unsigned)((elems + 7) / 8), 256, 0, st>>>(part, splits, g.co, Kp, g.k, g.c, c_real,
+                                                                          w, vel, gw, wp, b, vb, gb, lr, mu);
 }
 
-inline void launch_im2col_packed(const bf16* x, const ConvGeom& g, int c_real, int Kp, bf16* xcol, cudaStream_t st) {
+template <class T>
+inline void launch_im2col_packed(const T* x, const ConvGeom& g, int c_real, int Kp, T* xcol, cudaStream_t st) {
   const size_t total = (size_t)g.n * g.oh * g.ow * (Kp / 8);
-  im2col_packed_kernel<<<grid_for(total), 256, 0, st>>>(x, g, c_real, Kp, FastDiv(Kp / 8), FastDiv(g.ow),
-                                                        FastDiv(g.oh), xcol);
+  im2col_packed_kernel<T><<<grid_for(total), 256, 0, st>>>(x, g, c_real, Kp, FastDiv(Kp / 8), FastDiv(g.ow),
+                                                           FastDiv(g.oh), xcol);
+}
+
+// fp32 check mode: the same packed GEMMs on CUDA cores (simt_gemm over plain operands)
+inline void conv_fwd_packed_simt(const ConvGeom& g, const float* xcol, int Kp, const float* wpf, const float* bias,
+                                 int relu, float* y, cudaStream_t st) {
+  const int M = g.n * g.oh * g.ow;
+  simt_gemm(DenseXA<float>{xcol, Kp}, FwdB{wpf, Kp}, FwdEpi<float>{y, bias, g.co, relu != 0}, M, g.co, Kp, 1, st);
+}
+inline void conv_wgrad_packed_simt(const ConvGeom& g, const float* xcol, int Kp, const float* dy, float* part,
+                                   int splits, cudaStream_t st) {
+  const int Mo = g.n * g.oh * g.ow;
+  simt_gemm(WgradA<float>{dy, g.co}, DenseXN<float>{xcol, Kp}, PartialEpi{part, g.co, Kp}, g.co, Kp, Mo, splits, st);
 }
 
 }  // namespace ce

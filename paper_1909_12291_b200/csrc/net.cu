@@ -56,8 +56,9 @@ struct Layer {
   bool head = false;      // final Dense with <= kHeadMaxOut outputs: fused forward+loss / backward (head.cuh)
   bool packed = false;    // conv over channel-padded input without dX: packed im2col GEMMs (first_layer_tc.cuh)
   int Kp = 0;             // packed: im2col row width
-  bf16* Wp = nullptr;     // packed: bf16 mirror [co][Kp]
-  bf16* xcol = nullptr;   // packed: im2col matrix [B*oh*ow][Kp] of the last forward
+  bf16* Wp = nullptr;     // packed (bf16 mode): bf16 mirror [co][Kp]
+  float* Wpf = nullptr;   // packed (fp32 check mode): fp32 mirror [co][Kp]
+  void* xcol = nullptr;   // packed: im2col matrix [B*oh*ow][Kp] (activation type) of the last forward
   bf16* Wbp = nullptr;    // dense: bf16 mirror [out][in_pad]
   bf16* x16 = nullptr;    // dense after dense: bf16 copy of the fp32 input [B][in_pad]
   int in_pad = 0, out_pad = 0;
@@ -327,10 +328,14 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
       Prof pf(net, P_CONV_FWD, 2.0 * M * g.co * g.k * g.k * l.c_real,
               ab * ((double)n * g.h * g.w * g.c + (double)M * g.co + (double)g.co * K) + 4.0 * g.co);
       if (l.packed) {
-        launch_im2col_packed((const bf16*)in, g, l.c_real, l.Kp, l.xcol, st);
+        launch_im2col_packed((const T*)in, g, l.c_real, l.Kp, (T*)l.xcol, st);
         CE_CHECK_LAUNCH();
-        int s = conv_fwd_packed(g, l.xcol, l.Kp, l.Wp, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
-        if (s != CE_OK) return s;
+        if (net->use_tc) {
+          int s = conv_fwd_packed(g, (const bf16*)l.xcol, l.Kp, l.Wp, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
+          if (s != CE_OK) return s;
+        } else {
+          conv_fwd_packed_simt(g, (const float*)l.xcol, l.Kp, l.Wpf, l.b, l.relu, (float*)l.out, st);
+        }
       } else if (net->use_tc) {
         int s = conv_fwd_tc(g, (const bf16*)in, l.Wbf, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
         if (s != CE_OK) return s;
@@ -524,8 +529,13 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       int splits;
       {
       Prof pf(net, P_CONV_WGRAD, useful, ab * ((double)Mo * g.co + (double)n * g.h * g.w * g.c));
-      if (l.packed) {
-        int s = conv_wgrad_packed(g, l.xcol, l.Kp, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
+      if (l.packed && !net->use_tc) {
+        const long long Mo_ = (long long)n * g.oh * g.ow;
+        splits = simt_splits((int)Mo_, pick_splits(simt_tiles(g.co, l.Kp), Mo_, 512, net->num_sms));
+        while (splits > 1 && (size_t)splits * g.co * l.Kp * 4 > net->ws_bytes) splits = simt_splits((int)Mo_, splits - 1);
+        conv_wgrad_packed_simt(g, (const float*)l.xcol, l.Kp, (const float*)dy, net->ws, splits, st);
+      } else if (l.packed) {
+        int s = conv_wgrad_packed(g, (const bf16*)l.xcol, l.Kp, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
         pf.bytes = ab * ((double)Mo * g.co + (double)Mo * l.Kp) + 4.0 * splits * g.co * l.Kp;
       } else if (net->use_tc) {
@@ -543,8 +553,12 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       }
       if (l.packed) {  // bias gradient = row Kr of the packed wgrad: no column-sum pass
         Prof pf(net, P_CONV_SGD, 0.0, 4.0 * splits * g.co * l.Kp + 20.0 * g.co * (packed_kr(g, l.c_real) + 1));
-        launch_conv_sgd_packed(net->ws, splits, g, l.c_real, l.Kp, l.W, l.VW, keep ? l.GW : nullptr, l.Wp, l.b, l.Vb,
-                               keep ? l.Gb : nullptr, lr, mu, st);
+        if (l.Wpf)
+          launch_conv_sgd_packed(net->ws, splits, g, l.c_real, l.Kp, l.W, l.VW, keep ? l.GW : nullptr, l.Wpf, l.b,
+                                 l.Vb, keep ? l.Gb : nullptr, lr, mu, st);
+        else
+          launch_conv_sgd_packed(net->ws, splits, g, l.c_real, l.Kp, l.W, l.VW, keep ? l.GW : nullptr, l.Wp, l.b,
+                                 l.Vb, keep ? l.Gb : nullptr, lr, mu, st);
         CE_CHECK_LAUNCH();
         if (!l.need_dx) break;
         cur ^= 1;
@@ -869,13 +883,18 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         int sp = simt_splits((int)Mo, pick_splits(bps, Mo, 512, net->num_sms));
         sp = std::max(sp, conv_wgrad_tc_max_splits(l.g, (int)B, net->num_sms));
         ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);
-        l.packed = net->use_tc && l.c_real < l.g.c && !l.need_dx && !packed_disabled() &&
+        l.packed = (net->use_tc || precision == CE_PREC_FP32) && l.c_real < l.g.c && !l.need_dx && !packed_disabled() &&
                    packed_kp(l.g, l.c_real) <= kPackedMaxKp && Mo * packed_kp(l.g, l.c_real) / 8 < (1ll << 32);
         if (l.packed) {
           l.Kp = packed_kp(l.g, l.c_real);
           const int psp = conv_wgrad_packed_splits(l.Kp, (int)Mo, net->num_sms);
           ws = std::max(ws, (size_t)psp * l.g.co * l.Kp * 4);
-          ALLOC(l.xcol, (size_t)Mo * l.Kp * 2);
+          ALLOC(l.xcol, (size_t)Mo * l.Kp * ab);
+          if (precision == CE_PREC_FP32) {
+            ALLOC(l.Wpf, (size_t)l.g.co * l.Kp * 4);
+            ws = std::max(ws, (size_t)simt_splits((int)Mo, pick_splits(simt_tiles(l.g.co, l.Kp), Mo, 512,
+                                                                         net->num_sms)) * l.g.co * l.Kp * 4);
+          }
         }
       }
     }
@@ -984,6 +1003,9 @@ int ce_net_set_params(ce_net* net, int p, const float* w, const float* b) {
   if (l.Wp)
     pack_first_w_kernel<<<grid_for((size_t)l.g.co * l.Kp), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.c, l.c_real, l.Kp,
                                                                          l.Wp);
+  if (l.Wpf)
+    pack_first_w_kernel<<<grid_for((size_t)l.g.co * l.Kp), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.c, l.c_real, l.Kp,
+                                                                         l.Wpf);
   CE_CHECK_LAUNCH();
   CE_CUDA(cudaStreamSynchronize(st));
   return CE_OK;
@@ -1029,6 +1051,9 @@ int ce_net_init_uniform(ce_net* net, int p, uint64_t st_hi, uint64_t st_lo, uint
   if (l.Wp)
     pack_first_w_kernel<<<grid_for((size_t)l.g.co * l.Kp), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.c, l.c_real, l.Kp,
                                                                          l.Wp);
+  if (l.Wpf)
+    pack_first_w_kernel<<<grid_for((size_t)l.g.co * l.Kp), 256, 0, st>>>(l.W, l.g.co, l.g.k, l.g.c, l.c_real, l.Kp,
+                                                                         l.Wpf);
   CE_CHECK_LAUNCH();
   // no host buffers involved: the draws stay stream-ordered before the net's next
   // work (training / forward on the same stream), so no synchronisation here
