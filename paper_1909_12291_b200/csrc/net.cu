@@ -1122,8 +1122,10 @@ int ce_net_forward_host(ce_net* net, const float* x, int n, float* logits) {
   if (n < 1 || n > net->max_batch) return fail(CE_EINVAL, "batch %d outside [1, %d]", n, net->max_batch);
   DevGuard dg(net->device);
   SharedGate gate(net->device);
+  net->acc = 0;
   if (int s = upload_host_batch(net, x, n)) return s;
   if (int s = forward_any(net, n)) return s;
+  g_launches += net->acc;
   if (logits)
     CE_CUDA(cudaMemcpyAsync(logits, net->L.back().out, (size_t)n * net->classes * 4, cudaMemcpyDeviceToHost, net->st));
   CE_CUDA(cudaStreamSynchronize(net->st));
@@ -1172,7 +1174,9 @@ int ce_net_train_batch_host(ce_net* net, const float* x, const int64_t* labels, 
   if (int s = upload_host_batch(net, x, n)) return s;
   CE_CUDA(cudaMemcpyAsync(net->ybatch, y.data(), n * 4, cudaMemcpyHostToDevice, net->st));
   CE_CUDA(cudaMemsetAsync(net->d_step, 0, 4, net->st));
+  net->acc = 0;
   if (int s = step_any(net, n, lr, momentum)) return s;
+  g_launches += net->acc;
   CE_CUDA(cudaMemcpyAsync(loss, net->d_losses, 4, cudaMemcpyDeviceToHost, net->st));
   CE_CUDA(cudaStreamSynchronize(net->st));
   return CE_OK;
