@@ -21,6 +21,7 @@
 #include "dense_simt.cuh"
 #include "first_layer_tc.cuh"
 #include "head.cuh"
+#include "col2im_tc.cuh"
 #include "init.cuh"
 
 namespace ce {
@@ -55,6 +56,7 @@ struct Layer {
   bf16 *Wbf = nullptr, *Wtbf = nullptr;
   bool head = false;      // final Dense with <= kHeadMaxOut outputs: fused forward+loss / backward (head.cuh)
   bool packed = false;    // conv over channel-padded input without dX: packed im2col GEMMs (first_layer_tc.cuh)
+  bool col2im = false;    // stride-1 few-channel dgrad as GEMM + col2im (col2im_tc.cuh)
   int Kp = 0;             // packed: im2col row width
   bf16* Wp = nullptr;     // packed (bf16 mode): bf16 mirror [co][Kp]
   float* Wpf = nullptr;   // packed (fp32 check mode): fp32 mirror [co][Kp]
@@ -114,6 +116,7 @@ struct ce_net {
   bf16* gbf = nullptr;  // bf16 copy of a dense output gradient [B][out_pad]
   size_t gbytes = 0;
   float* ws = nullptr;
+  bf16* zbuf = nullptr;  // col2im dgrad: Z [pixels][k*k*C] of the largest eligible layer
   size_t ws_bytes = 0;
   int* d_step = nullptr;   // [0] step counter, [1] non-finite flag
   int* h_flags = nullptr;  // pinned: non-finite flag snapshots of in-flight chunks
@@ -518,7 +521,9 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         Prof pf(net, P_CONV_DGRAD, useful,
                 ab * ((double)Mo * g.co + (double)g.co * K + 2.0 * n * g.h * g.w * g.c));
         if (net->use_tc) {
-          int s = conv_dgrad_tc(g, (const bf16*)dy, l.Wtbf, (const bf16*)mask, (bf16*)gout, net->num_sms, st);
+          int s = l.col2im ? conv_dgrad_col2im(g, (const bf16*)dy, l.Wbf, (const bf16*)mask, (bf16*)gout, net->zbuf,
+                                             net->num_sms, st)
+                         : conv_dgrad_tc(g, (const bf16*)dy, l.Wtbf, (const bf16*)mask, (bf16*)gout, net->num_sms, st);
           if (s != CE_OK) return s;
         } else {
           simt_gemm(make_dgrad_a(dy, g), DgradB{l.W, g}, DgradEpi<T>{(T*)gout, mask, g.c}, n * g.h * g.w, g.c,
@@ -842,7 +847,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
     if (l.kind == CE_LAYER_DENSE) total_params += (size_t)l.out_units * l.in_units;
   }
   net->keep_grads = false;  // opt-in (ce_net_keep_grads): storing dW costs 4 B/param/step
-  size_t max_g = (size_t)B * net->in_cp * net->in_h * net->in_w * ab, ws = 0, gbf_elems = 0;
+  size_t max_g = (size_t)B * net->in_cp * net->in_h * net->in_w * ab, ws = 0, gbf_elems = 0, zbytes = 0;
   for (size_t i = 0; i < net->L.size(); ++i) {
     Layer& l = net->L[i];
     if (l.kind == CE_LAYER_DENSE) {
@@ -883,6 +888,8 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         int sp = simt_splits((int)Mo, pick_splits(bps, Mo, 512, net->num_sms));
         sp = std::max(sp, conv_wgrad_tc_max_splits(l.g, (int)B, net->num_sms));
         ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);
+        l.col2im = net->use_tc && l.need_dx && col2im_dgrad_eligible(l.g);
+        if (l.col2im) zbytes = std::max(zbytes, col2im_dgrad_zbytes(l.g, (int)B));
         l.packed = (net->use_tc || precision == CE_PREC_FP32) && l.c_real < l.g.c && !l.need_dx && !packed_disabled() &&
                    packed_kp(l.g, l.c_real) <= kPackedMaxKp && Mo * packed_kp(l.g, l.c_real) / 8 < (1ll << 32);
         if (l.packed) {
@@ -927,6 +934,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
   net->gbytes = max_g;
   ALLOC(net->ws, ws);
   net->ws_bytes = ws;
+  if (zbytes) ALLOC(net->zbuf, zbytes);
   if (gbf_elems) ALLOC(net->gbf, gbf_elems * 2);
   ALLOC(net->d_step, 16);  // [0] step, [1] non-finite flag, [2] head ticket
   cudaMemsetAsync(net->d_step, 0, 16, net->st);
