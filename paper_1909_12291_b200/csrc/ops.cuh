@@ -198,7 +198,7 @@ constexpr int kPoolStrip = 8;
 constexpr size_t kPoolStripMinWork = (size_t)148 * 2048 * 8;  // >= 8 strip rows per resident thread
 
 template <class T, int K, int S>
-__global__ void __launch_bounds__(256) maxpool_fwd_strip_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y,
+__global__ void __launch_bounds__(256, K == 2 ? 4 : 2) maxpool_fwd_strip_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y,
                                                                 uint8_t* __restrict__ arg, bool relu_flag) {
   const int cg = g.c / 8, strips = (g.oh + kPoolStrip - 1) / kPoolStrip;
   const int total = g.n * strips * g.ow * cg;
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(256) maxpool_fwd_strip_kernel(const T* __restr
 // stride-1 backward: input row r receives from window rows p in [r-K+1, r]; the
 // thread keeps those K rows (dy + argmax of its K window columns) in a ring
 template <class T, class TG, int K>
-__global__ void __launch_bounds__(256) maxpool_bwd_s1_strip_kernel(const TG* __restrict__ dy,
+__global__ void __launch_bounds__(256, K == 2 ? 4 : 2) maxpool_bwd_s1_strip_kernel(const TG* __restrict__ dy,
                                                                    const uint8_t* __restrict__ arg, ConvGeom g,
                                                                    const T* __restrict__ mask, TG* __restrict__ dx) {
   const int cg = g.c / 8, strips = (g.h + kPoolStrip - 1) / kPoolStrip;
