@@ -168,6 +168,8 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):  # diagnostics only: the contract requires the sample
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
