@@ -213,6 +213,9 @@ struct FwdTcLoader {
 
 struct FwdTcEpi {
   static constexpr bool STAGED_BF16 = true;  // coalesced row stores through shared memory (tc_engine)
+  // pure-TMA loaders (1 producer warp) leave room for 16 epilogue warps: the bf16
+  // store stream is the limit of the wide forwards (gather loaders keep 8: registers)
+  static constexpr int EPI_WARPS_TMA = 16;
   bf16* y;
   const float* bias;
   int M, co, relu;

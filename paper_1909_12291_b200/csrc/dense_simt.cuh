@@ -137,6 +137,93 @@ __global__ void __launch_bounds__(256, R == 4 ? 3 : 2)
   }
 }
 
+// Strip variant of the dW + SGD pass for wide layers: a CTA owns a 64-column
+// strip of W, stages x[:, strip] in shared memory ONCE, and walks its range of
+// rows in 64-row chunks (g staged per chunk). The per-tile kernel above refills
+// the same x strip for every 16-row tile, which costs as much L2->SM traffic as
+// W itself. Thread (cq = tid % 16, rg = tid / 16) owns 4 rows x 4 columns per
+// chunk; accumulation order (b ascending) is the tile kernel's, so the results
+// are bit-identical. grid (in / 64, row splits); in % 4 == 0, x_ld % 4 == 0.
+constexpr int DSS_TI = 64, DSS_TR = 64, DSS_MAXB = 64;
+template <class TX>
+__global__ void __launch_bounds__(256)
+    dense_dw_sgd_strip_kernel(const TX* __restrict__ x, int x_ld, const float* __restrict__ g, int B, int in,
+                              int out, int rows_per_split, float* __restrict__ w, float* __restrict__ vel,
+                              float* __restrict__ gw, bf16* __restrict__ wb, int wb_ld, float lr, float mu) {
+  extern __shared__ __align__(16) float dss_smem[];
+  float* Xs = dss_smem;               // [B][64]
+  float* Gs = dss_smem + B * DSS_TI;  // [B][64]
+  const int cq = threadIdx.x & 15, rg = threadIdx.x >> 4;
+  const int ib = blockIdx.x * DSS_TI, i0 = ib + cq * 4;
+  const bool colok = i0 < in;  // in % 4 == 0: a quad is all in or all out
+  for (int e = threadIdx.x; e < B * (DSS_TI / 4); e += 256) {
+    const int bb = e / (DSS_TI / 4), q = e % (DSS_TI / 4), i = ib + q * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < in) v = ld4f(x + (size_t)bb * x_ld + i);
+    *(float4*)&Xs[bb * DSS_TI + q * 4] = v;
+  }
+  const int o_begin = blockIdx.y * rows_per_split, o_end = min(out, o_begin + rows_per_split);
+  for (int oc = o_begin; oc < o_end; oc += DSS_TR) {
+    const int o0 = oc + rg * 4;
+    float4 pw[4], pv[4];
+    if (w && colok) {  // the update's operands, in flight during the staging and FMA loop
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (o0 + r < o_end) {
+          pw[r] = __ldcs((const float4*)(w + (size_t)(o0 + r) * in + i0));
+          pv[r] = __ldcs((const float4*)(vel + (size_t)(o0 + r) * in + i0));
+        }
+    }
+    __syncthreads();  // previous chunk's Gs reads done (first pass: Xs staged)
+    for (int e = threadIdx.x; e < B * DSS_TR; e += 256) {
+      const int bb = e / DSS_TR, oo = e % DSS_TR, o = oc + oo;
+      Gs[bb * DSS_TR + oo] = o < o_end ? g[(size_t)bb * out + o] : 0.f;
+    }
+    __syncthreads();
+    float acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = 0.f;
+#pragma unroll 4
+    for (int bb = 0; bb < B; ++bb) {
+      const float4 xv = *(const float4*)&Xs[bb * DSS_TI + cq * 4];
+      const float4 gv = *(const float4*)&Gs[bb * DSS_TR + rg * 4];
+      const float gr[4] = {gv.x, gv.y, gv.z, gv.w};
+      fma_rx4<4>(acc, gr, xv);
+    }
+    if (!colok) continue;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int o = o0 + r;
+      if (o >= o_end) break;
+      const size_t off = (size_t)o * in + i0;
+      if (gw) __stcs((float4*)(gw + off), make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]));
+      if (!w) continue;
+      sgd_update(pw[r].x, pv[r].x, acc[r][0], lr, mu);
+      sgd_update(pw[r].y, pv[r].y, acc[r][1], lr, mu);
+      sgd_update(pw[r].z, pv[r].z, acc[r][2], lr, mu);
+      sgd_update(pw[r].w, pv[r].w, acc[r][3], lr, mu);
+      __stcs((float4*)(w + off), pw[r]);
+      __stcs((float4*)(vel + off), pv[r]);
+      if (wb) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(pw[r].x, pw[r].y),
+                             hi = __floats2bfloat162_rn(pw[r].z, pw[r].w);
+        uint2 u;
+        u.x = *(const uint32_t*)&lo;
+        u.y = *(const uint32_t*)&hi;
+        *(uint2*)(wb + (size_t)o * wb_ld + i0) = u;
+      }
+    }
+  }
+}
+
+inline bool dense_dw_strip_disabled() {  // CE_DENSE_DW_STRIP=0: per-tile kernel (comparison)
+  static const bool off = [] {
+    const char* e = getenv("CE_DENSE_DW_STRIP");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 // dX[b][i] = sum_o g[b][o] w[o][i] (pre-update weights), gated by (mask > 0).
 // grid (cdiv(B, 32), cdiv(in, 256)): blocks sharing a W tile run back to back.
 template <class TO, class TM>
@@ -286,34 +373,38 @@ __global__ void __launch_bounds__(256, 2)
 
 // Split-K dense forward on CUDA cores (fp32 check mode, small batch):
 // part[split][b][o] = sum over the split's k-range of x[b][k] W[o][k].
-// Block = 256 outputs x 32 rows, 256 threads: lane -> 8 outputs (o = lane + 32 j),
-// warp -> 4 rows. W is staged [o][k] with a 33-float stride (conflict-free fill
+// Block = 64R outputs x 32 rows, 256 threads: warp w takes rows 8 (w % 4) .. +7
+// and output half w / 4; lane -> R outputs (o = half * 32R + lane + 32 j). Each
+// W value read from shared memory (per-lane rows: 4 wavefronts per float4)
+// feeds 8 rows of FMAs -- at 4 rows per thread the W reads alone saturate
+// shared memory. W is staged [o][k] with a 36-float stride (conflict-free fill
 // from float4 rows and conflict-free per-lane reads), x is staged [k][b] and
 // read as warp-uniform float4 broadcasts; the next K chunk is fetched into
 // registers while the current one is consumed (one barrier per chunk).
 constexpr int DF_TB = 32, DF_KC = 32, DF_WS = DF_KC + 4, DF_XS = DF_TB + 4;
 template <int R>
-constexpr int df_smem() { return 2 * (32 * R * DF_WS + DF_KC * DF_XS) * 4; }
-// R outputs per lane: block tile 32R outputs (R chosen per layer to limit padding)
+constexpr int df_smem() { return 2 * (64 * R * DF_WS + DF_KC * DF_XS) * 4; }
+// R outputs per lane: block tile 64R outputs (R chosen per layer to limit padding)
 template <class TX, int R>
 __global__ void __launch_bounds__(256, 2) dense_fwd_simt_kernel(const TX* __restrict__ x, const float* __restrict__ w,
                                                                 int B, int in, int out, int kchunk,
                                                                 float* __restrict__ part) {
-  constexpr int DF_TO = 32 * R;
+  constexpr int DF_TO = 64 * R;
   extern __shared__ __align__(16) float dsm[];
   // buffer b: W at dsm + b * DF_TO * DF_WS, x at xs0 + b * DF_KC * DF_XS
   float* const xs0 = dsm + 2 * DF_TO * DF_WS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rgp = warp & 3, oh = warp >> 2;
   const int ob = blockIdx.x * DF_TO, bb = blockIdx.y * DF_TB;
   const int k0 = blockIdx.z * kchunk, k1 = min(in, k0 + kchunk);
   const bool kvec = (in & 3) == 0;
-  // fetch mapping: W: 8 float4 per thread (row = tid/8 + 32 i, kq = tid % 8); x: 1 float4 (b = tid/8)
+  // fetch mapping: W: 2R float4 per thread (row = tid/8 + 32 i, kq = tid % 8); x: 1 float4 (b = tid/8)
   const int frow = tid >> 3, fkq = tid & 7;
-  float4 rw[R], rx;
+  float4 rw[2 * R], rx;
   auto fetch = [&](int kc) {
     const int k = kc + fkq * 4;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
+    for (int i = 0; i < 2 * R; ++i) {
       const int o = ob + frow + 32 * i;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (o < out) {
@@ -341,14 +432,16 @@ __global__ void __launch_bounds__(256, 2) dense_fwd_simt_kernel(const TX* __rest
   };
   auto stash = [&](int buf) {
 #pragma unroll
-    for (int i = 0; i < R; ++i)
+    for (int i = 0; i < 2 * R; ++i)
       *(float4*)(dsm + buf * (DF_TO * DF_WS) + (frow + 32 * i) * DF_WS + fkq * 4) = rw[i];
     float* d = xs0 + buf * (DF_KC * DF_XS) + (fkq * 4) * DF_XS + frow;
     d[0] = rx.x; d[DF_XS] = rx.y; d[2 * DF_XS] = rx.z; d[3 * DF_XS] = rx.w;
   };
-  float acc[R][4];
+  float acc[R][8];
 #pragma unroll
-  for (int j = 0; j < R; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[j][r] = 0.f;
   if (k0 < k1) {
     fetch(k0);
     stash(0);
@@ -358,24 +451,22 @@ __global__ void __launch_bounds__(256, 2) dense_fwd_simt_kernel(const TX* __rest
   for (int kc = k0; kc < k1; kc += DF_KC) {
     const bool more = kc + DF_KC < k1;
     if (more) fetch(kc + DF_KC);
-    const float* W = dsm + buf * (DF_TO * DF_WS);
-    const float* X = xs0 + buf * (DF_KC * DF_XS);
+    const float* W = dsm + buf * (DF_TO * DF_WS) + (oh * 32 * R + lane) * DF_WS;
+    const float* X = xs0 + buf * (DF_KC * DF_XS) + rgp * 8;
 #pragma unroll 2
     for (int kk = 0; kk < DF_KC; kk += 4) {
-      // W rows (stride 36 floats: the 8 lanes of a phase hit distinct bank quads)
       float4 wq[R];
 #pragma unroll
-      for (int j = 0; j < R; ++j) wq[j] = *(const float4*)(W + (lane + 32 * j) * DF_WS + kk);
+      for (int j = 0; j < R; ++j) wq[j] = *(const float4*)(W + 32 * j * DF_WS + kk);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float4 xv = *(const float4*)(X + (kk + u) * DF_XS + warp * 4);
+        const float4 xa = *(const float4*)(X + (kk + u) * DF_XS), xb = *(const float4*)(X + (kk + u) * DF_XS + 4);
+        const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
 #pragma unroll
         for (int j = 0; j < R; ++j) {
           const float wv = u == 0 ? wq[j].x : u == 1 ? wq[j].y : u == 2 ? wq[j].z : wq[j].w;
-          acc[j][0] = fmaf(xv.x, wv, acc[j][0]);
-          acc[j][1] = fmaf(xv.y, wv, acc[j][1]);
-          acc[j][2] = fmaf(xv.z, wv, acc[j][2]);
-          acc[j][3] = fmaf(xv.w, wv, acc[j][3]);
+#pragma unroll
+          for (int r = 0; r < 8; ++r) acc[j][r] = fmaf(xv[r], wv, acc[j][r]);
         }
       }
     }
@@ -385,12 +476,12 @@ __global__ void __launch_bounds__(256, 2) dense_fwd_simt_kernel(const TX* __rest
   }
   float* dst = part + (size_t)blockIdx.z * B * out;
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int b = bb + warp * 4 + r;
+  for (int r = 0; r < 8; ++r) {
+    const int b = bb + rgp * 8 + r;
     if (b >= B) break;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      const int o = ob + lane + 32 * j;
+      const int o = ob + oh * 32 * R + lane + 32 * j;
       if (o < out) dst[(size_t)b * out + o] = acc[j][r];
     }
   }
@@ -407,17 +498,17 @@ inline bool dense_fwd_simt_enabled() {
 
 // outputs per lane minimising padded outputs (ties -> larger tiles)
 inline int dense_fwd_simt_r(int out) {
-  int best = 8;
+  int best = 4;
   long long best_pad = -1;
-  for (int r : {8, 6, 4}) {
-    const long long pad = (long long)((out + 32 * r - 1) / (32 * r)) * 32 * r;
+  for (int r : {4, 3, 2}) {
+    const long long pad = (long long)((out + 64 * r - 1) / (64 * r)) * 64 * r;
     if (best_pad < 0 || pad < best_pad) best_pad = pad, best = r;
   }
   return best;
 }
 
 inline int dense_fwd_simt_splits(int B, int in, int out, int num_sms) {
-  const int to = 32 * dense_fwd_simt_r(out);
+  const int to = 64 * dense_fwd_simt_r(out);
   const long long blocks = (long long)((out + to - 1) / to) * ((B + DF_TB - 1) / DF_TB);
   long long s = (2LL * num_sms + blocks - 1) / blocks;
   const long long cap = (in + 255) / 256;
@@ -432,7 +523,7 @@ inline int dense_fwd_simt_r_launch(const TX* x, const float* w, int B, int in, i
   cudaFuncSetAttribute(dense_fwd_simt_kernel<TX, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, df_smem<R>());
   const int kchunk = ((in + splits - 1) / splits + DF_KC - 1) / DF_KC * DF_KC;
   const int s = (in + kchunk - 1) / kchunk;
-  dim3 grid((out + 32 * R - 1) / (32 * R), (B + DF_TB - 1) / DF_TB, s);
+  dim3 grid((out + 64 * R - 1) / (64 * R), (B + DF_TB - 1) / DF_TB, s);
   dense_fwd_simt_kernel<TX, R><<<grid, 256, df_smem<R>(), st>>>(x, w, B, in, out, kchunk, part);
   return s;
 }
@@ -441,9 +532,9 @@ template <class TX>
 inline int dense_fwd_simt(const TX* x, const float* w, int B, int in, int out, int splits, float* part,
                           cudaStream_t st) {
   switch (dense_fwd_simt_r(out)) {
-    case 4: return dense_fwd_simt_r_launch<TX, 4>(x, w, B, in, out, splits, part, st);
-    case 6: return dense_fwd_simt_r_launch<TX, 6>(x, w, B, in, out, splits, part, st);
-    default: return dense_fwd_simt_r_launch<TX, 8>(x, w, B, in, out, splits, part, st);
+    case 2: return dense_fwd_simt_r_launch<TX, 2>(x, w, B, in, out, splits, part, st);
+    case 3: return dense_fwd_simt_r_launch<TX, 3>(x, w, B, in, out, splits, part, st);
+    default: return dense_fwd_simt_r_launch<TX, 4>(x, w, B, in, out, splits, part, st);
   }
 }
 
@@ -461,7 +552,11 @@ inline bool dense_dw_simt_enabled(int B) {
     const char* e = getenv("CE_DENSE_DW_TC");
     return e && e[0] == '1';
   }();
-  return !force_tc && B <= kDenseDwSimtMaxBatchBf16;
+  static const int maxb = [] {  // CE_DENSE_DW_SIMT_MAXB=N moves the crossover (measurement)
+    const char* e = getenv("CE_DENSE_DW_SIMT_MAXB");
+    return e ? atoi(e) : kDenseDwSimtMaxBatchBf16;
+  }();
+  return !force_tc && B <= maxb;
 }
 
 inline int dense_dw_rows() {  // rows per thread (CE_DENSE_DW_ROWS = 4 | 8)
@@ -475,6 +570,18 @@ inline int dense_dw_rows() {  // rows per thread (CE_DENSE_DW_ROWS = 4 | 8)
 template <class TX>
 inline void dense_dw_sgd_simt(const TX* x, int x_ld, const float* g, int B, int in, int out, float* w, float* vel,
                               float* gw, bf16* wb, int wb_ld, float lr, float mu, cudaStream_t st) {
+  if (!dense_dw_strip_disabled() && (in & 3) == 0 && (x_ld & 3) == 0 && B <= DSS_MAXB) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int strips = cdiv(in, DSS_TI), chunks = cdiv(out, DSS_TR);
+    const int splits = std::max(1, std::min(chunks, cdiv(6 * sms, strips)));  // >= ~6 CTAs per SM
+    const int rows = cdiv(chunks, splits) * DSS_TR;
+    const int smem = 2 * B * DSS_TI * (int)sizeof(float);
+    dense_dw_sgd_strip_kernel<TX><<<dim3(strips, cdiv(out, rows)), 256, smem, st>>>(
+        x, x_ld, g, B, in, out, rows, w, vel, gw, wb, wb_ld, lr, mu);
+    return;
+  }
   if (dense_dw_rows() == 8) {
     dim3 grid(cdiv(in, DS_TI), cdiv(out, 32));
     dense_dw_sgd_simt_kernel<TX, 8><<<grid, 256, 0, st>>>(x, x_ld, g, B, in, out, w, vel, gw, wb, wb_ld, lr, mu);

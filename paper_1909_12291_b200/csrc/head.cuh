@@ -53,41 +53,72 @@ __global__ void __launch_bounds__(256) head_fwd_kernel(const TX* __restrict__ x,
   }
   __syncthreads();
   const bool vec = ((x_ld & 7) == 0) && ((i0 & 7) == 0);  // 8 consecutive columns per lane
-  for (int b = b_lo + warp; b < b_hi; b += 8) {
-    float acc[OUT];
+  // two rows per warp pass (b, b + 8): 8 x-vector loads in flight per lane
+  for (int b = b_lo + warp; b < b_hi; b += 16) {
+    const bool two = b + 8 < b_hi;
+    float acc[2][OUT];
 #pragma unroll
-    for (int o = 0; o < OUT; ++o) acc[o] = 0.f;
-    const TX* xr = x + (size_t)b * x_ld + i0;
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int o = 0; o < OUT; ++o) acc[r][o] = 0.f;
+    const TX* xr0 = x + (size_t)b * x_ld + i0;
+    const TX* xr1 = x + (size_t)(two ? b + 8 : b) * x_ld + i0;
     if (vec) {
       const int n8 = n & ~7;
-      for (int i = lane * 8; i < n8; i += 256) {
-        float xv[8];
-        load8(xr + i, xv);
+      for (int i = lane * 8; i < n8; i += 4 * 256) {
+        float xv[2][4][8];
 #pragma unroll
-        for (int o = 0; o < OUT; ++o) {
-          const float4 wa = *(const float4*)&Ws[o][i], wb = *(const float4*)&Ws[o][i + 4];
-          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        for (int q = 0; q < 4; ++q)
+          if (i + q * 256 < n8) {
+            load8(xr0 + i + q * 256, xv[0][q]);
+            if (two) load8(xr1 + i + q * 256, xv[1][q]);
+          }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc[o] = fmaf(xv[u], wv[u], acc[o]);
+        for (int q = 0; q < 4; ++q) {
+          if (i + q * 256 >= n8) break;
+          const int iq = i + q * 256;
+#pragma unroll
+          for (int o = 0; o < OUT; ++o) {
+            const float4 wa = *(const float4*)&Ws[o][iq], wb = *(const float4*)&Ws[o][iq + 4];
+            const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[0][o] = fmaf(xv[0][q][u], wv[u], acc[0][o]);
+            if (two) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) acc[1][o] = fmaf(xv[1][q][u], wv[u], acc[1][o]);
+            }
+          }
         }
       }
       for (int i = n8 + lane; i < n; i += 32) {
-        const float xv = ldf(xr, i);
+        const float x0 = ldf(xr0, i), x1 = ldf(xr1, i);
 #pragma unroll
-        for (int o = 0; o < OUT; ++o) acc[o] = fmaf(xv, Ws[o][i], acc[o]);
+        for (int o = 0; o < OUT; ++o) {
+          acc[0][o] = fmaf(x0, Ws[o][i], acc[0][o]);
+          acc[1][o] = fmaf(x1, Ws[o][i], acc[1][o]);
+        }
       }
     } else {
       for (int i = lane; i < n; i += 32) {
-        const float xv = ldf(xr, i);
+        const float x0 = ldf(xr0, i), x1 = ldf(xr1, i);
 #pragma unroll
-        for (int o = 0; o < OUT; ++o) acc[o] = fmaf(xv, Ws[o][i], acc[o]);
+        for (int o = 0; o < OUT; ++o) {
+          acc[0][o] = fmaf(x0, Ws[o][i], acc[0][o]);
+          acc[1][o] = fmaf(x1, Ws[o][i], acc[1][o]);
+        }
       }
     }
 #pragma unroll
-    for (int o = 0; o < OUT; ++o) {
+    for (int r = 0; r < 2; ++r) {
+      if (r == 1 && !two) break;
+      const int br = b + 8 * r;
 #pragma unroll
-      for (int m = 16; m > 0; m >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], m);
-      if (lane == 0) partial[((size_t)blockIdx.x * B + b) * OUT + o] = acc[o];
+      for (int o = 0; o < OUT; ++o) {
+        float v = acc[r][o];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        if (lane == 0) partial[(size_t)(br * OUT + o) * gridDim.x + blockIdx.x] = v;
+      }
     }
   }
   __threadfence();
@@ -96,13 +127,25 @@ __global__ void __launch_bounds__(256) head_fwd_kernel(const TX* __restrict__ x,
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // one warp per logit: lanes take strided CTAs, fixed xor tree (deterministic)
-  for (int e = warp; e < B * OUT; e += 8) {
-    float s = 0.f;
-    for (int c = lane; c < (int)gridDim.x; c += 32) s += __ldcg(partial + (size_t)c * B * OUT + e);
+  const int G = (int)gridDim.x, E = B * OUT;
+  // [logit][cta] partials, lanes over consecutive CTAs; 8 logits per warp at once
+  // (8 independent loads per lane per step), each summed in CTA order then by a
+  // fixed xor tree (deterministic)
+  for (int e0 = warp * 8; e0 < E; e0 += 64) {
+    float s[8];
 #pragma unroll
-    for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-    if (lane == 0) logits[e] = s + bias[e % OUT];
+    for (int j = 0; j < 8; ++j) s[j] = 0.f;
+    for (int c = lane; c < G; c += 32) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (e0 + j < E) s[j] += __ldcg(partial + (size_t)(e0 + j) * G + c);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], m);
+      if (lane == 0 && e0 + j < E) logits[e0 + j] = s[j] + bias[(e0 + j) % OUT];
+    }
   }
   if (threadIdx.x == 0) *ticket = 0u;  // ready for the next launch / graph replay
   if (!labels) return;
@@ -144,6 +187,15 @@ __global__ void __launch_bounds__(256) head_fwd_kernel(const TX* __restrict__ x,
   }
 }
 
+__device__ __forceinline__ void st4(float* p, const float (&v)[4]) { *(float4*)p = make_float4(v[0], v[1], v[2], v[3]); }
+__device__ __forceinline__ void st4(bf16* p, const float (&v)[4]) {
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+  uint2 u;
+  u.x = *(const uint32_t*)&lo;
+  u.y = *(const uint32_t*)&hi;
+  *(uint2*)p = u;
+}
+
 // one thread per 4 consecutive input columns; grid cdiv(in, 1024)
 template <class TX, class TD, int OUT>
 __global__ void __launch_bounds__(256) head_bwd_kernel(const TX* __restrict__ x, int x_ld, const float* __restrict__ g,
@@ -170,6 +222,7 @@ __global__ void __launch_bounds__(256) head_bwd_kernel(const TX* __restrict__ x,
   const int nj = min(4, in - i0);
   const bool wvec = ((in & 3) == 0) && nj == 4;
   const bool xvec = ((x_ld & 3) == 0) && nj == 4;
+  const bool mask_x = mask && (const void*)mask == (const void*)x && x_ld == in;
   float wv[OUT][4], vv[OUT][4], acc[OUT][4];
 #pragma unroll
   for (int o = 0; o < OUT; ++o) {
@@ -210,12 +263,19 @@ __global__ void __launch_bounds__(256) head_bwd_kernel(const TX* __restrict__ x,
     }
     if (dx) {
       const size_t off = (size_t)r * in + i0;
+      if (mask_x && xvec) {  // the ReLU mask is this layer's input: reuse xv, one vector store
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (j >= nj) break;
-        float v = d[j];
-        if (mask && !(ldf(mask, off + j) > 0.f)) v = 0.f;
-        stf(dx, off + j, v);
+        for (int j = 0; j < 4; ++j)
+          if (!(xv[j] > 0.f)) d[j] = 0.f;
+        st4(dx + off, d);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j >= nj) break;
+          float v = d[j];
+          if (mask && !(ldf(mask, off + j) > 0.f)) v = 0.f;
+          stf(dx, off + j, v);
+        }
       }
     }
   }

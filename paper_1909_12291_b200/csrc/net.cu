@@ -918,7 +918,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
           ALLOC(l.Wp, (size_t)l.g.co * l.Kp * 2);
         } else {
           ALLOC(l.Wbf, l.wn * 2);
-          ALLOC(l.Wtbf, l.wn * 2);
+          if (!l.col2im) ALLOC(l.Wtbf, l.wn * 2);  // col2im dgrad reads the forward mirror
         }
       }
       cudaMemsetAsync(l.W, 0, l.wn * 4, net->st);

@@ -624,14 +624,76 @@ __global__ void __launch_bounds__(256) conv_sgd_warp_kernel(
     }
   }
 }
+// Many splits over a mid-sized layer: one thread per float4 of weights, splits
+// summed in order (loads coalesced across lanes); trailing blocks reduce the bias
+// with one warp per channel. The dgrad transpose (if any) is written per element.
+__global__ void __launch_bounds__(256) conv_sgd_vec_kernel(
+    const float* __restrict__ part, int splits, int co, int K, int cp, int k, int s, float* __restrict__ w,
+    float* __restrict__ vel, float* __restrict__ gw, bf16* __restrict__ wbf, bf16* __restrict__ wtbf,
+    const float* __restrict__ bpart, int bsplits, float* __restrict__ b, float* __restrict__ vb,
+    float* __restrict__ gb, float lr, float mu, unsigned eblocks) {
+  const size_t total = (size_t)co * K;
+  if (blockIdx.x >= eblocks) {  // bias: one warp per channel
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int o = (int)(blockIdx.x - eblocks) * 8 + warp;
+    if (!bpart || o >= co) return;
+    const float g = warp_sum_splits(bpart, bsplits, co, o);
+    if (lane == 0) {
+      if (gb) gb[o] = g;
+      if (b) {
+        float bv = b[o], v = vb[o];
+        sgd_update(bv, v, g, lr, mu);
+        b[o] = bv;
+        vb[o] = v;
+      }
+    }
+    return;
+  }
+  const size_t e = ((size_t)blockIdx.x * 256 + threadIdx.x) * 4;  // K % 4 == 0
+  if (e >= total) return;
+  float4 g = *(const float4*)(part + e);
+#pragma unroll 4
+  for (int sp = 1; sp < splits; ++sp) g = f4add(g, *(const float4*)(part + (size_t)sp * total + e));
+  if (gw) *(float4*)(gw + e) = g;
+  if (!w) return;
+  float4 wv = *(const float4*)(w + e), vv = *(const float4*)(vel + e);
+  sgd_update(wv.x, vv.x, g.x, lr, mu);
+  sgd_update(wv.y, vv.y, g.y, lr, mu);
+  sgd_update(wv.z, vv.z, g.z, lr, mu);
+  sgd_update(wv.w, vv.w, g.w, lr, mu);
+  *(float4*)(w + e) = wv;
+  *(float4*)(vel + e) = vv;
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(wv.x, wv.y), hi = __floats2bfloat162_rn(wv.z, wv.w);
+  if (wbf) {
+    uint2 u;
+    u.x = *(const uint32_t*)&lo;
+    u.y = *(const uint32_t*)&hi;
+    *(uint2*)(wbf + e) = u;
+  }
+  if (wtbf) {
+    const bf16 v4[4] = {lo.x, lo.y, hi.x, hi.y};
+    for (int j = 0; j < 4; ++j) {
+      const size_t ej = e + j;
+      const int o = (int)(ej / K), kk = (int)(ej % K), c = kk % cp, tap = kk / cp;
+      wtbf[dg_wt_index(k, s, cp, co, tap / k, tap % k, c, o)] = v4[j];
+    }
+  }
+}
+
 inline void launch_conv_sgd(const float* part, int splits, int co, int K, int cp, int k, int s, float* w, float* vel,
                             float* gw, bf16* wbf, bf16* wtbf, const float* bpart, int bsplits, float* b, float* vb,
                             float* gb, float lr, float mu, cudaStream_t st) {
-  if (splits > 16) {  // many splits = small layer: one warp per element
-    const size_t total = (size_t)co * K;
+  const size_t total = (size_t)co * K;
+  if (splits > 16 && total <= 16384) {  // many splits over a tiny layer: one warp per element
     const unsigned blocks = (unsigned)((total + 7) / 8 + (co + 7) / 8);
     conv_sgd_warp_kernel<<<blocks, 256, 0, st>>>(part, splits, co, K, cp, k, s, w, vel, gw, wbf, wtbf, bpart, bsplits,
                                                  b, vb, gb, lr, mu);
+    return;
+  }
+  if (splits > 16) {  // many splits, more elements: a thread per float4, splits in order
+    const unsigned eblocks = (unsigned)((total / 4 + 255) / 256);
+    conv_sgd_vec_kernel<<<eblocks + (unsigned)((co + 7) / 8), 256, 0, st>>>(
+        part, splits, co, K, cp, k, s, w, vel, gw, wbf, wtbf, bpart, bsplits, b, vb, gb, lr, mu, eblocks);
     return;
   }
   dim3 grid((K + CS_TK - 1) / CS_TK, (co + CS_TO - 1) / CS_TO);

@@ -54,10 +54,21 @@ struct EpiStaged : std::false_type {};
 template <class Epi>
 struct EpiStaged<Epi, std::void_t<decltype(Epi::STAGED_BF16)>> : std::bool_constant<Epi::STAGED_BF16> {};
 
+// Epi::EPI_WARPS_TMA: epilogue warps when the loader is pure TMA (one producer warp)
+template <class Epi, class = void>
+struct EpiWarpsTma {
+  static constexpr int value = 0;
+};
+template <class Epi>
+struct EpiWarpsTma<Epi, std::void_t<decltype(Epi::EPI_WARPS_TMA)>> {
+  static constexpr int value = Epi::EPI_WARPS_TMA;
+};
+
 template <class Loader, class Epi>
 struct TcRoles {
   static constexpr int PW = ProducerWarps<Loader>::value;
-  static constexpr int EW = EpiWarps<Epi>::value;
+  static constexpr int EW =
+      (Loader::PURE_TMA && EpiWarpsTma<Epi>::value) ? EpiWarpsTma<Epi>::value : EpiWarps<Epi>::value;
   static constexpr int MMA_WARP = PW + EW;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static_assert(EW % 4 == 0, "epilogue warps must cover the 4 TMEM lane quarters equally");
@@ -119,7 +130,9 @@ struct TcSmemLayout {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196 * 1024 / STAGE_BYTES) > 8 ? 8 : (196 * 1024 / STAGE_BYTES);
+  // pipeline budget: 196 KB less any epilogue staging beyond the 8 KB of 8 staged warps
+  static constexpr int RING = 196 * 1024 - (EPI_STAGE > 8192 ? EPI_STAGE - 8192 : 0);
+  static constexpr int STAGES = (RING / STAGE_BYTES) > 8 ? 8 : (RING / STAGE_BYTES);
   static constexpr int LAG = STAGES - 1 > TC_MAX_LAG ? TC_MAX_LAG : STAGES - 1;  // cp.async groups in flight
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
