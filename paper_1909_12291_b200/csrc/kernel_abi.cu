@@ -192,7 +192,7 @@ int ce_gather_u8_normalize(const uint8_t* pixels, int c, int h, int w, const int
     return fail(CE_EINVAL, "bad gather arguments (n=%d c=%d c_store=%d)", n, c, c_store);
   cudaStream_t st = (cudaStream_t)stream;
   const int HW = h * w;
-  dim3 grid(cdiv(HW, 256), n);
+  dim3 grid = gather_grid(HW, n);
   if (precision == CE_PREC_BF16)
     gather_u8_kernel<bf16><<<grid, 256, 0, st>>>(pixels, nullptr, idx, nullptr, 0, 0, 0, n, c, c_store, HW, (bf16*)out,
                                                  nullptr);

@@ -618,7 +618,7 @@ int step_any(ce_net* net, int n, float lr, float mu) {
 
 int gather_any(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm, int spe, int base, int B,
                bool labels) {
-  dim3 grid(cdiv(ds->h * ds->w, 256), B);
+  dim3 grid = gather_grid(ds->h * ds->w, B);
   int HW = ds->h * ds->w;
   Prof pf(net, P_GATHER, 0.0, (double)B * HW * (ds->c + net->in_cp * act_bytes(net)));
   if (net->prec == CE_PREC_FP32)
@@ -1384,7 +1384,7 @@ int ce_predict_stream(ce_net* net, const uint8_t* pixels, long long count, int b
     CE_CUDA(cudaMemcpyAsync(r.stage[b], pixels + (size_t)start * img, img * nb, cudaMemcpyHostToDevice, r.cs));
     CE_CUDA(cudaEventRecord(copied[b], r.cs));
     CE_CUDA(cudaStreamWaitEvent(st, copied[b], 0));
-    dim3 grid(cdiv(HW, 256), nb);
+    dim3 grid = gather_grid(HW, nb);
     if (net->prec == CE_PREC_FP32)
       gather_u8_kernel<float><<<grid, 256, 0, st>>>(r.stage[b], nullptr, nullptr, nullptr, 0, 0, 0, nb, net->in_c,
                                                     net->in_cp, HW, (float*)net->x0, nullptr);

@@ -25,11 +25,21 @@ __device__ __forceinline__ void store8(T* p, const float (&v)[8]);
 // x[b][y][x][cp] = cp < C ? pix[idx[b]][cp][y][x] / 255 : 0      (data.py:65-66)
 // idx source: perm[epoch*n_perm + bi*B + b] with (epoch, bi) from the device
 // step counter (graph-replayable), or a plain base index (predict).
+// One thread per 4 consecutive pixels: one 4-byte load per channel plane and
+// 4 x (Cp/8) 16-byte stores; the correctly rounded v/255 (true division, as
+// numpy's astype(f32)/f32(255)) comes from a 256-entry shared table.
+constexpr int kGatherPx = 4;
+inline dim3 gather_grid(int HW, int B) { return dim3((unsigned)((HW + kGatherPx * 256 - 1) / (kGatherPx * 256)), B); }
+
 template <class T>
-__global__ void gather_u8_kernel(const uint8_t* __restrict__ pix, const uint8_t* __restrict__ labels,
-                                 const int32_t* __restrict__ perm, const int* __restrict__ step_ctr, int n_perm,
-                                 int steps_per_epoch, int base, int B, int C, int Cp, int HW, T* __restrict__ x,
-                                 int32_t* __restrict__ y) {
+__global__ void __launch_bounds__(256) gather_u8_kernel(const uint8_t* __restrict__ pix,
+                                                        const uint8_t* __restrict__ labels,
+                                                        const int32_t* __restrict__ perm,
+                                                        const int* __restrict__ step_ctr, int n_perm,
+                                                        int steps_per_epoch, int base, int B, int C, int Cp, int HW,
+                                                        T* __restrict__ x, int32_t* __restrict__ y) {
+  __shared__ float lut[256];
+  lut[threadIdx.x] = __fdiv_rn((float)threadIdx.x, 255.0f);  // blockDim.x == 256
   const int b = blockIdx.y;
   int src;
   if (perm && step_ctr) {
@@ -41,18 +51,41 @@ __global__ void gather_u8_kernel(const uint8_t* __restrict__ pix, const uint8_t*
   } else {
     src = base + b;
   }
+  __syncthreads();
   const uint8_t* img = pix + (size_t)src * C * HW;
-  for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < HW; px += gridDim.x * blockDim.x) {
-    T* dst = x + ((size_t)b * HW + px) * Cp;
-    // 8 channels per vector store (Cp % 8 == 0): one 16-byte (bf16) / 2x16-byte (fp32) store
-    for (int c0 = 0; c0 < Cp; c0 += 8) {
-      float v[8];
+  T* xb = x + (size_t)b * HW * Cp;
+  if ((HW & 3) == 0 && (reinterpret_cast<uintptr_t>(pix) & 3) == 0) {
+    const int HW4 = HW >> 2;
+    for (int p4 = blockIdx.x * blockDim.x + threadIdx.x; p4 < HW4; p4 += gridDim.x * blockDim.x) {
+      for (int c0 = 0; c0 < Cp; c0 += 8) {
+        float v[kGatherPx][8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = c0 + u;
-        v[u] = c < C ? __fdiv_rn((float)img[(size_t)c * HW + px], 255.0f) : 0.f;
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u;
+          if (c < C) {
+            const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(img + (size_t)c * HW) + p4);
+#pragma unroll
+            for (int k = 0; k < kGatherPx; ++k) v[k][u] = lut[(q >> (8 * k)) & 0xff];
+          } else {
+#pragma unroll
+            for (int k = 0; k < kGatherPx; ++k) v[k][u] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kGatherPx; ++k) store8(xb + ((size_t)p4 * kGatherPx + k) * Cp + c0, v[k]);
       }
-      store8(dst + c0, v);
+    }
+  } else {
+    for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < HW; px += gridDim.x * blockDim.x) {
+      for (int c0 = 0; c0 < Cp; c0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = c0 + u;
+          v[u] = c < C ? lut[img[(size_t)c * HW + px]] : 0.f;
+        }
+        store8(xb + (size_t)px * Cp + c0, v);
+      }
     }
   }
   if (y && labels && blockIdx.x == 0 && threadIdx.x == 0) y[b] = labels[src];
