@@ -1,0 +1,72 @@
+"""C3: the steady-state multi-objective GA, population 64 x 5
+generations (= 320 evaluations), with the population evaluated across the GPUs
+of one box by the process-per-GPU pull scheduler (scheduler.ProcessGpuPool:
+one gpu_worker process per GPU, `--slots` socket workers each).
+
+    python tools/ga_run.py [--gpus N] [--slots K] [--evals 320] [--out log.jsonl]
+
+Prints one JSON line: candidates/h over the whole run (wall clock of the
+master, worker-process start-up included), best genome and fitness, failures,
+per-worker busy fractions. The master is the
+reference's (ga.Master: evolution.py:99-186); selection is bit-exact given the
+arrival order of the records, which pull scheduling makes run-dependent, so
+the best genome can differ between runs (as in the reference's WorkerPool).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1909_12291_b200 import EvolutionSettings, Master, ObjectiveConfig, SearchSpace  # noqa: E402
+from paper_1909_12291_b200.ga import JsonlLog  # noqa: E402
+from paper_1909_12291_b200.genes import format_genome  # noqa: E402
+from paper_1909_12291_b200.scheduler import ProcessGpuPool  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--slots", type=int, default=4)
+    ap.add_argument("--capacity", type=int, default=64)
+    ap.add_argument("--evals", type=int, default=320)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--out", default=None, help="JSONL audit log of the master")
+    a = ap.parse_args()
+    obj = {"kind": "measured_latency", "alpha": -0.2, "lo": 1e-5, "hi": 1e-2}
+    config = {"budget": {"epochs": 2}, "objective": obj, "seed": 0, "precision": "bf16"}
+    log = JsonlLog(a.out) if a.out else None
+    master = Master(SearchSpace(), ObjectiveConfig(**obj),
+                    EvolutionSettings(capacity=a.capacity, elite_count=2, tournament_size=3, crossover_prob=0.5,
+                                      max_evaluations=a.evals), seed=a.seed, log=log)
+    failures = []
+    collect = master.collect
+
+    def counted(record):
+        if not record.ok:
+            failures.append(record.failure_reason)
+        collect(record)
+    master.collect = counted
+    pool = ProcessGpuPool(master, config, devices=tuple(range(a.gpus)), slots_per_gpu=a.slots, order="fifo")
+    t0 = time.perf_counter()
+    report = pool.run()
+    wall = time.perf_counter() - t0
+    if log:
+        log.close()
+    best = master.best
+    busy = {w: round(s.busy_time_s / max(wall, 1e-9), 3) for w, s in sorted(report.stats.items())}
+    print(json.dumps({
+        "config": "C3 steady-state GA", "gpus": a.gpus, "slots_per_gpu": a.slots, "capacity": a.capacity,
+        "evaluations": master.completed, "wall_s": round(wall, 3),
+        "candidates_per_h": master.completed / wall * 3600.0,
+        "note": "wall clock includes worker-process start-up (CUDA context + library load per GPU)",
+        "failures": len(failures), "failure_reasons": sorted(set(map(str, failures)))[:8],
+        "best_genome": format_genome(best.genome) if best else None,
+        "best_fitness": best.record.fitness if best and best.record.ok else None,
+        "protocol_errors": master.protocol_errors, "worker_busy_frac": busy}))
+
+
+if __name__ == "__main__":
+    main()
