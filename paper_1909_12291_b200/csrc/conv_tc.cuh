@@ -736,6 +736,11 @@ inline int conv_wgrad_splits(const ConvGeom& g, int n, int num_sms) {
   if (want > nkb / 4) want = nkb / 4;
   if (want > 128) want = 128;
   if (want < 1) want = 1;
+  static const int forced = [] {  // CE_WGRAD_SPLITS=N: measurement override
+    const char* e = getenv("CE_WGRAD_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) want = std::min<long long>(forced, std::max<long long>(1, nkb));
   return (int)want;
 }
 inline int conv_wgrad_tc_max_splits(const ConvGeom& g, int n, int num_sms) { return conv_wgrad_splits(g, n, num_sms); }
