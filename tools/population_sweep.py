@@ -63,6 +63,15 @@ def main():
         dist.barrier()
     else:
         ts = [t]
+    import collections
+    reasons = collections.Counter(" ".join(str(r.failure_reason).split()[:3]) for r in recs
+                                  if r is not None and not r.ok)
+    from paper_1909_12291_b200.genes import format_genome
+    byid = {g.id: g for g in mine}
+    top = sorted(report.trace, key=lambda t: t[2] - t[3])[:4]
+    print(json.dumps({"rank": rank, "failure_reasons": reasons.most_common(6),
+                      "longest": [[round(b - a, 3), format_genome(byid[gid])] for gid, _, a, b in top]}),
+          file=sys.stderr, flush=True)
     if rank == 0:
         per = [x.tolist() for x in ts]
         tmax = max(p[0] for p in per)
