@@ -141,6 +141,18 @@ int dev_alloc(ce_net* net, void** p, size_t bytes) {
   if (bytes == 0) bytes = 16;
   bytes = (bytes + 255) & ~(size_t)255;
   cudaError_t e = cudaMallocAsync(p, bytes, net->st);
+  if (e == cudaErrorMemoryAllocation) {
+    // the pool keeps freed memory cached (keep_pool_memory): after a giant
+    // candidate it can be held in blocks of the wrong size, so hand the unused
+    // part back to the driver and retry once before reporting OOM
+    cudaGetLastError();
+    int dev = 0;
+    cudaMemPool_t pool;
+    cudaStreamSynchronize(net->st);
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(p, bytes, net->st);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(CE_ENOMEM, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
