@@ -736,6 +736,19 @@ inline int conv_wgrad_splits(const ConvGeom& g, int n, int num_sms) {
   if (want > nkb / 4) want = nkb / 4;
   if (want > 128) want = 128;
   if (want < 1) want = 1;
+  if (nkb / want >= 256) {
+    // long splits: wave balance outweighs the per-split fixed cost, so allow a few
+    // (nearly full) waves; each extra wave is charged 4% (measured on SWEET:
+    // 4 splits = 128/148 SMs 684 TF/s, 9 splits = 288/296 790 TF/s, 13 = 416/444 696 TF/s)
+    double best = 0.0;
+    long long pick = want;
+    for (long long s = want; s <= 128 && s <= nkb / 64; ++s) {
+      const long long units = (long long)m_tiles * s, waves = (units + num_sms - 1) / num_sms;
+      const double score = (double)units / (double)(waves * num_sms) * (1.0 - 0.04 * (double)(waves - 1));
+      if (score > best + 1e-9) best = score, pick = s;
+    }
+    want = pick;
+  }
   static const int forced = [] {  // CE_WGRAD_SPLITS=N: measurement override
     const char* e = getenv("CE_WGRAD_SPLITS");
     return e ? atoi(e) : 0;
