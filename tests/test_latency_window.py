@@ -36,3 +36,31 @@ def test_flush_completes_records_in_place():
     fv = score(0.5, raw, obj)
     assert (rec.objective_raw, rec.objective_m, rec.fitness) == (raw, fv.m, fv.f)
     assert not w.pending
+
+
+class _SizedDev(_Dev):
+    def __init__(self, nbytes):
+        self.nbytes = nbytes
+
+    def device_bytes(self):
+        return self.nbytes
+
+
+class _SizedNet(_Net):
+    def __init__(self, nbytes):
+        self.device_net = _SizedDev(nbytes)
+
+
+def test_window_caps_held_device_bytes():
+    """Past the cap a candidate is measured at once (C5: 512 deferred nets on one GPU)."""
+    w = LatencyWindow(cap_bytes=100)
+    assert w.try_reserve(_SizedNet(60))
+    assert not w.try_reserve(_SizedNet(50))   # 110 > 100: measure inline
+    assert w.try_reserve(_SizedNet(40))       # exactly at the cap
+    assert w.held_bytes == 100 and w.measured_inline == 1
+    w.flush()
+    assert w.held_bytes == 0 and w.try_reserve(_SizedNet(90))
+
+
+def test_window_measures_inline_without_size():
+    assert not LatencyWindow().try_reserve(_Net())  # no device_bytes(): never defer blindly
