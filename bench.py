@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--slots", type=int, default=4, help="candidates packed per GPU (streams)")
     ap.add_argument("--order", choices=["lpt", "two_ended", "fifo"], default="two_ended",
                     help="dispatch order of the pre-issued population")
+    ap.add_argument("--big-slots", type=int, default=1,
+                    help="two_ended: slots per GPU that take the longest remaining candidate")
     ap.add_argument("--precision", choices=["bf16", "fp32"], default="bf16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -259,7 +261,7 @@ def main():
     def step(profile=False):
         recs, report = evaluate_population(mine, splits, budget, obj, seed=0, devices=(device,),
                                            slots_per_gpu=1 if profile else args.slots, precision=args.precision,
-                                           profile=profile, order=args.order)
+                                           profile=profile, order=args.order, big_slots=args.big_slots)
         last_trace[:] = getattr(report, "trace", [])
         last_window[0] = getattr(report, "latency_window_s", 0.0)
         return recs

@@ -66,7 +66,7 @@ class ListMaster:
 
 
 def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), slots_per_gpu=2,
-                        order="two_ended", precision="bf16", defer_latency=True, **evaluate_kwargs):
+                        order="two_ended", precision="bf16", defer_latency=True, big_slots=1, **evaluate_kwargs):
     """Evaluate every genome; returns (records in input order, PoolReport).
 
     order "two_ended" (default): slot 0 of each GPU takes the longest remaining
@@ -85,7 +85,7 @@ def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), 
         return evaluate(genome, splits, budget, objective, seed, worker_id=worker_id,
                         precision=precision, device=device, latency_window=window, **evaluate_kwargs)
 
-    pool = GpuPool(run_one, master, devices=devices, slots_per_gpu=slots_per_gpu, order=order,
+    pool = GpuPool(run_one, master, devices=devices, slots_per_gpu=slots_per_gpu, order=order, big_slots=big_slots,
                    cost_fn=lambda g: estimate_cost(g, n_train, budget))
     report = pool.run()
     report.trace = pool.trace
