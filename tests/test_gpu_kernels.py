@@ -109,3 +109,34 @@ def test_pool_exact(size, stride, variant, precision):
         assert rel(dx, dx_ref) <= 1e-6
     else:  # overlapping windows accumulate in fp32 then round to bf16
         assert rel(dx, dx_ref) <= 1e-2
+
+
+def test_wgrad_multiwave_splits():
+    """Long reductions take the multi-wave split count (conv_wgrad_splits: 8x256x94x94 k4 has
+    32 M tiles and 1,036 k-blocks -> 9 splits, 288 units on 148 SMs); checked against a
+    PyTorch fp32 (no TF32) weight gradient on the same bf16 operands."""
+    n, c, h, co, k, s = 8, 256, 94, 256, 4, 1
+    oh = h - k + 1
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n, c, h, h, device="cuda", generator=g).to(torch.bfloat16)
+    dy = torch.randn(n, co, oh, oh, device="cuda", generator=g).to(torch.bfloat16)
+    prev = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        dw_ref = torch.nn.grad.conv2d_weight(x.float(), (co, c, k, k), dy.float(), stride=s)
+    finally:
+        torch.backends.cudnn.allow_tf32 = prev
+    desc = native.conv_desc(n, c, h, h, co, k, s, "bf16")
+    xd = x.permute(0, 2, 3, 1).contiguous()
+    dyd = dy.permute(0, 2, 3, 1).contiguous()
+    dwd = torch.empty((co, k, k, c), dtype=torch.float32, device="cuda")
+    dbd = torch.empty(co, dtype=torch.float32, device="cuda")
+    wsb = native.conv_workspace_bytes(desc)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    native.conv_wgrad(desc, xd.data_ptr(), dyd.data_ptr(), dwd.data_ptr(), dbd.data_ptr(), ws.data_ptr(), wsb, st)
+    torch.cuda.synchronize()
+    dw = dwd.permute(0, 3, 1, 2).cpu().numpy()
+    assert rel(dw, dw_ref.cpu().numpy()) <= 1e-2, f"wgrad rel err {rel(dw, dw_ref.cpu().numpy()):.3e}"
+    db_ref = dy.float().sum(dim=(0, 2, 3)).cpu().numpy()
+    assert rel(dbd.cpu().numpy(), db_ref) <= 1e-2
