@@ -120,8 +120,11 @@ int ce_net_get_grads(ce_net* net, int p, float* gw, float* gb);
 
 /* inference forward of n samples (float32 NCHW host) -> logits (n, classes) */
 int ce_net_forward_host(ce_net* net, const float* x, int n, float* logits);
-/* output of layer `layer` (descriptor index) from the last forward, NCHW / (n, units) float32 */
+/* output of layer `layer` (descriptor index) from the last forward, NCHW / (n, units) float32;
+ * CE_EINVAL for a conv whose max-pool runs in its epilogue (not materialised) */
 int ce_net_get_activation(ce_net* net, int layer, int n, float* out);
+/* *yes = 0 when layer `layer` is a conv fused with the following max-pool (bf16, non-overlapping window) */
+int ce_net_layer_materialized(const ce_net* net, int layer, int* yes);
 /* one SGD step on a host batch; writes the pre-step mean loss */
 int ce_net_train_batch_host(ce_net* net, const float* x, const int64_t* labels, int n, float lr, float momentum,
                             float* loss);
@@ -162,8 +165,13 @@ typedef struct ce_conv_desc {
 } ce_conv_desc;
 
 size_t ce_conv_workspace_bytes(const ce_conv_desc* d);
-int ce_conv_fwd(const ce_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
-                void* stream);
+/* y = conv(x, w) + bias, ReLU if relu (nn.py:82-94, 178-180).
+ * pool_k > 0: max-pool epilogue (MaxPool.forward, nn.py:140-150) for a
+ * non-overlapping window (pool_k in {2, 3}, pool_s >= pool_k; bf16 only): y is
+ * the POOLED map [n][ph][pw][c_out] and arg its u8 argmax (row-major first
+ * max; 0xFF = dead window when relu), the pre-pool map is never written.      */
+int ce_conv_fwd(const ce_conv_desc* d, const void* x, const void* w, const float* bias, int relu, int pool_k,
+                int pool_s, void* y, uint8_t* arg, void* stream);
 /* dx = conv^T(dy, w), optionally gated by (mask > 0) -- the ReLU backward of the
  * layer that produced the conv input (nn.py:182-183)                          */
 int ce_conv_dgrad(const ce_conv_desc* d, const void* dy, const void* w, const void* mask, void* dx, void* workspace,
@@ -243,6 +251,10 @@ int ce_prof_num_classes(void);
 int ce_net_set_profiling(ce_net* net, int on);
 int ce_net_prof_read(ce_net* net, int cls, const char** name, long long* launches, double* ms, double* flops,
                      double* bytes);
+/* roofline time of a class: sum over its launches of max(flops / P, bytes / BW), P and BW set process-wide by
+ * ce_prof_set_peaks (bench.py passes MEASURED_PEAKS.json's sustained bf16 FLOP/s and HBM bytes/s) */
+int ce_prof_set_peaks(double flops_per_s, double bytes_per_s);
+int ce_net_prof_ideal(ce_net* net, int cls, double* ideal_ms);
 
 #ifdef __cplusplus
 }

@@ -111,10 +111,62 @@ inline bool narrow_im2col_enabled() {
   return e && e[0] == '1';
 }
 
+// ------------------------------------------------------------------ pooled row order
+// A conv whose output feeds a non-overlapping max-pool (stride >= window,
+// nn.py:119-150) runs its GEMM rows in WINDOW-MAJOR order, so the epilogue sees
+// every pool window inside one warp and emits the pooled value + argmax
+// directly (FwdPoolEpi): the pre-pool activation is never written. Row r of
+// tile t: warp quarter wq = r / 32, lane l = r % 32 -> window
+// t*WPT + wq*WPW + l / KK, tap l % KK (row-major inside the window, the
+// reference's first-max order); lanes >= WPW*KK of a quarter are padding.
+// Conv outputs no window covers (stride > window gaps, ragged edges) are never
+// computed: the reference routes them a zero gradient (nn.py:156-167).
+struct PoolMap {
+  int KK, WPW, WPT;  // taps per window; windows per 32-row warp quarter / per 128-row tile
+  int ps, pst;       // pool window and stride
+  int windows;       // n * PH * PW = pooled pixels
+  FastDiv d_pw, d_ph, d_kk, d_ps;
+  // conv output pixel (n, p, q) of row r of tile t; false for a padding row
+  __device__ __forceinline__ bool pixel(int t, int r, uint32_t& n, uint32_t& p, uint32_t& q) const {
+    uint32_t wl, tap;
+    d_kk.divmod((uint32_t)(r & 31), wl, tap);
+    if ((int)wl >= WPW) return false;
+    const int window = t * WPT + (r >> 5) * WPW + (int)wl;
+    if (window >= windows) return false;
+    uint32_t rest, pw, ph, di, dj;
+    d_pw.divmod((uint32_t)window, rest, pw);
+    d_ph.divmod(rest, n, ph);
+    d_ps.divmod(tap, di, dj);
+    p = ph * pst + di;
+    q = pw * pst + dj;
+    return true;
+  }
+};
+
+inline PoolMap make_pool_map(int n, int oh, int ow, int ps, int pst) {
+  PoolMap pm{};
+  const int PH = (oh - ps) / pst + 1, PW = (ow - ps) / pst + 1;
+  pm.ps = ps;
+  pm.pst = pst;
+  pm.KK = ps * ps;
+  pm.WPW = 32 / pm.KK;
+  pm.WPT = 4 * pm.WPW;
+  pm.windows = n * PH * PW;
+  pm.d_pw = FastDiv(PW);
+  pm.d_ph = FastDiv(PH);
+  pm.d_kk = FastDiv(pm.KK);
+  pm.d_ps = FastDiv(ps);
+  return pm;
+}
+// GEMM rows of the pooled order (whole 128-row tiles)
+inline int pool_rows(const PoolMap& pm) { return (pm.windows + pm.WPT - 1) / pm.WPT * TC_BM; }
+inline bool pool_fusable(int ps, int pst) { return (ps == 2 || ps == 3) && pst >= ps; }
+
 // ------------------------------------------------------------------ forward
 // table: xoff[k8] = im2col offset of K chunk k8 = (tap, c0) relative to the
 // output pixel's receptive-field origin: (i*W + j)*C + c0.
-template <int MODE>
+// POOL: rows in the window-major order of `pm` (gather modes 0 / 1 only).
+template <int MODE, bool POOL = false>
 struct FwdTcLoader {
   // MODE 0: cp.async gather A + cp.async B; 1: gather A + TMA B;
   //      2: TMA im2col A (64-channel slabs, SW128) + TMA B;
@@ -129,6 +181,8 @@ struct FwdTcLoader {
   ConvGeom g;
   int K, M, BN;
   FastDiv d_ow, d_oh;
+  PoolMap pm;  // POOL
+  static_assert(!POOL || MODE <= 1, "the pooled row order needs the gather loader");
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
     if (IM2COL || NARROW) return;
     int* xoff = (int*)table;
@@ -183,11 +237,17 @@ struct FwdTcLoader {
     {
       const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;  // 256 producers: 2 threads per row
       const int m = c.m0 + r;
-      const bool row_ok = m < M;
       uint32_t q = 0, p = 0, n = 0, t = 0;
-      if (row_ok) {
-        d_ow.divmod((uint32_t)m, t, q);
-        d_oh.divmod(t, n, p);
+      bool row_ok;
+      if constexpr (POOL) {
+        row_ok = pm.pixel(c.m0 / TC_BM, r, n, p, q);
+        if (!row_ok) n = p = q = 0;
+      } else {
+        row_ok = m < M;
+        if (row_ok) {
+          d_ow.divmod((uint32_t)m, t, q);
+          d_oh.divmod(t, n, p);
+        }
       }
       const bf16* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
 #pragma unroll
@@ -267,6 +327,66 @@ struct FwdTcEpi {
   }
   __device__ void finish(int, int) const {}
 };
+
+// Pooled forward epilogue (rows in PoolMap order): bias + ReLU, rounded to the
+// bf16 the unfused path would store, then max + first-max argmax over the KK
+// lanes of each window by warp shuffles (maxpool_fwd_kernel's rule: a later tap
+// wins only if strictly greater; argmax kPoolDead when the window came out of a
+// ReLU and its max is not > 0). The window's tap-0 lane stores the pooled bf16
+// value and the u8 argmax in NHWC order of the pooled map.
+template <int KK>
+struct FwdPoolEpi {
+  static constexpr int WPW = 32 / KK;
+  bf16* y;       // pooled [windows][co]
+  uint8_t* arg;  // [windows][co]
+  const float* bias;
+  int co, relu;
+  PoolMap pm;
+  __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
+    const int lane = row & 31;
+    const int wl = lane / KK, tap = lane - wl * KK, base = wl * KK;
+    const int window = (c.m0 / TC_BM) * (4 * WPW) + (row >> 5) * WPW + wl;
+    const int o0 = c.n0 + col;
+    float best[16];
+    uint8_t bi[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float t = v[i] + (o0 + i < co ? __ldg(bias + o0 + i) : 0.f);
+      if (relu) t = t > 0.f ? t : 0.f;
+      t = __bfloat162float(__float2bfloat16_rn(t));
+      float bv = __shfl_sync(0xffffffffu, t, base);
+      int b = 0;
+#pragma unroll
+      for (int k = 1; k < KK; ++k) {
+        const float u = __shfl_sync(0xffffffffu, t, base + k);
+        if (u > bv) {
+          bv = u;
+          b = k;
+        }
+      }
+      best[i] = bv;
+      bi[i] = (relu && !(bv > 0.f)) ? kPoolDead : (uint8_t)b;
+    }
+    if (tap != 0 || wl >= WPW || window >= pm.windows || o0 >= co) return;
+    const size_t off = (size_t)window * co + o0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (o0 + 8 * h >= co) break;
+      __align__(16) bf16 out[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = __float2bfloat16_rn(best[8 * h + i]);
+      *(uint4*)(y + off + 8 * h) = *(const uint4*)out;
+      *(uint2*)(arg + off + 8 * h) = *(const uint2*)&bi[8 * h];
+    }
+  }
+  __device__ void finish(int, int) const {}
+};
+
+template <class Fn>
+inline int with_pool_kk(int ps, Fn&& fn) {
+  if (ps == 2) return fn(std::integral_constant<int, 4>());
+  return fn(std::integral_constant<int, 9>());
+}
 
 // ------------------------------------------------------------------ dgrad
 // Sub-pixel decomposition: input positions (h, w) = (rh + s*hh, rw + s*ww) of one
@@ -612,6 +732,40 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
       e = tc_launch<BN>(ld, ep, sh, num_sms, st);
     }
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc: %s", cudaGetErrorString(e));
+  });
+}
+
+// Conv forward + non-overlapping max-pool in one kernel (window-major rows,
+// FwdPoolEpi): y / arg are the POOLED map [n][PH][PW][co] and its argmax.
+inline int conv_fwd_tc_pool(const ConvGeom& g, const bf16* x, const bf16* w, const float* bias, int relu, int ps,
+                            int pst, bf16* y, uint8_t* arg, int num_sms, cudaStream_t st) {
+  if (!pool_fusable(ps, pst)) return fail(CE_EINVAL, "pool epilogue needs a non-overlapping 2x2 or 3x3 window");
+  const int K = g.k * g.k * g.c;
+  if ((K / 8) * 4 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_fwd_tc_pool: K=%d exceeds the chunk table", K);
+  const PoolMap pm = make_pool_map(g.n, g.oh, g.ow, ps, pst);
+  const int Mp = pool_rows(pm);
+  return with_bn(pick_bn(Mp / TC_BM, g.co, num_sms), [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    return with_pool_kk(ps, [&](auto kkc) {
+      constexpr int KK = decltype(kkc)::value;
+      TcShape sh = tc_make_shape(Mp, g.co, K, BN, 1);
+      FwdPoolEpi<KK> ep{y, arg, bias, g.co, relu, pm};
+      auto fill = [&](auto& ld) {
+        ld.x = x; ld.w = w; ld.g = g; ld.K = K; ld.M = Mp; ld.BN = BN; ld.pm = pm;
+        ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      };
+      cudaError_t e;
+      FwdTcLoader<1, true> ld1{};
+      if (!tma_disabled() && make_tmap_kmajor(&ld1.wmap, w, g.co, K, BN)) {
+        fill(ld1);
+        e = tc_launch<BN>(ld1, ep, sh, num_sms, st);
+      } else {
+        FwdTcLoader<0, true> ld0{};
+        fill(ld0);
+        e = tc_launch<BN>(ld0, ep, sh, num_sms, st);
+      }
+      return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc_pool: %s", cudaGetErrorString(e));
+    });
   });
 }
 

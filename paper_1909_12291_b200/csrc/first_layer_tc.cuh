@@ -36,11 +36,14 @@ inline int packed_kp(const ConvGeom& g, int c_real) { return (packed_kr(g, c_rea
 // Column kk reads x at (receptive-field origin) + off[kk]; off is built once per
 // block in shared memory (-1: the ones column, -2: zero padding); index math
 // is 32-bit with magic-number division.
+// POOL: rows in the window-major order of `pm` (conv_tc.cuh PoolMap); padding
+// rows are all zero, the ones column included, so they add nothing to the
+// packed wgrad (bias row) either.
 constexpr int kPackedMaxKp = 1024;
-template <class T>
+template <class T, bool POOL = false>
 __global__ void __launch_bounds__(256) im2col_packed_kernel(const T* __restrict__ x, ConvGeom g, int c_real,
                                                             int Kp, FastDiv d_chunks, FastDiv d_ow, FastDiv d_oh,
-                                                            T* __restrict__ xcol) {
+                                                            T* __restrict__ xcol, PoolMap pm, uint32_t rows) {
   __shared__ int off[kPackedMaxKp];
   const int Kr = g.k * g.k * c_real;
   for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
@@ -53,18 +56,28 @@ __global__ void __launch_bounds__(256) im2col_packed_kernel(const T* __restrict_
     }
   }
   __syncthreads();
-  const uint32_t total = (uint32_t)g.n * g.oh * g.ow * (uint32_t)(Kp / 8);
+  const uint32_t total = rows * (uint32_t)(Kp / 8);
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     uint32_t m, ch, t, q, p, n;
     d_chunks.divmod(e, m, ch);
-    d_ow.divmod(m, t, q);
-    d_oh.divmod(t, n, p);
-    const T* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
+    bool ok = true;
+    if constexpr (POOL) {
+      ok = pm.pixel((int)(m / TC_BM), (int)(m % TC_BM), n, p, q);
+    } else {
+      d_ow.divmod(m, t, q);
+      d_oh.divmod(t, n, p);
+    }
     float v[8];
+    if (ok) {
+      const T* base = x + (((size_t)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int o = off[ch * 8 + u];
-      v[u] = o >= 0 ? ldf(base, (size_t)o) : (o == -1 ? 1.f : 0.f);
+      for (int u = 0; u < 8; ++u) {
+        const int o = off[ch * 8 + u];
+        v[u] = o >= 0 ? ldf(base, (size_t)o) : (o == -1 ? 1.f : 0.f);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = 0.f;
     }
     store8(xcol + (size_t)m * Kp + ch * 8, v);  // bf16 values round-trip exactly
   }
@@ -101,6 +114,63 @@ inline int conv_fwd_packed(const ConvGeom& g, const bf16* xcol, int Kp, const bf
     cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_packed: %s", cudaGetErrorString(e));
   });
+}
+
+// Packed first conv + non-overlapping max-pool: xcol rows in PoolMap order
+// (launch_im2col_packed with the map), pooled epilogue.
+inline int conv_fwd_packed_pool(const ConvGeom& g, const bf16* xcol, int Kp, const bf16* wp, const float* bias,
+                                int relu, const PoolMap& pm, bf16* y, uint8_t* arg, int num_sms, cudaStream_t st) {
+  const int Mp = pool_rows(pm);
+  return with_bn(pick_bn(Mp / TC_BM, g.co, num_sms), [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    return with_pool_kk(pm.ps, [&](auto kkc) {
+      constexpr int KK = decltype(kkc)::value;
+      TcShape sh = tc_make_shape(Mp, g.co, Kp, BN, 1);
+      DenseFwdLoader ld{};
+      ld.BN = BN;
+      if (!make_tmap_kmajor(&ld.amap, xcol, Mp, Kp, TC_BM) || !make_tmap_kmajor(&ld.bmap, wp, g.co, Kp, BN))
+        return fail(CE_ECUDA, "conv_fwd_packed_pool: tensor map encoding failed");
+      FwdPoolEpi<KK> ep{y, arg, bias, g.co, relu, pm};
+      cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+      return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_packed_pool: %s", cudaGetErrorString(e));
+    });
+  });
+}
+
+// Backward of the fused pool for the packed layer, in the same window-major row
+// order as its xcol: dY[m][o] = dy_pooled[window][o] at the argmax tap, 0 at
+// the other taps, at dead windows and on padding rows (nn.py:156-167; stride
+// >= window, so every conv output has at most one window).
+template <class T>
+__global__ void __launch_bounds__(256) pool_expand_rows_kernel(const T* __restrict__ dyp, const uint8_t* __restrict__ arg,
+                                                               PoolMap pm, int co, uint32_t rows, T* __restrict__ dy) {
+  const int cg = co / 8;
+  const uint32_t total = rows * (uint32_t)cg;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t m = e / cg;
+    const int c0 = (int)(e - m * cg) * 8;
+    const int r = (int)(m % TC_BM), lane = r & 31;
+    const int wl = lane / pm.KK, tap = lane - wl * pm.KK;
+    const int window = (int)(m / TC_BM) * pm.WPT + (r >> 5) * pm.WPW + wl;
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (wl < pm.WPW && window < pm.windows) {
+      const size_t o = (size_t)window * co + c0;
+      float g[8];
+      load8(dyp + o, g);
+      const uint2 a2 = *(const uint2*)(arg + o);
+      const uint8_t* a = (const uint8_t*)&a2;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = a[u] == tap ? g[u] : 0.f;
+    }
+    store8(dy + (size_t)m * co + c0, v);
+  }
+}
+
+template <class T>
+inline void launch_pool_expand_rows(const T* dyp, const uint8_t* arg, const PoolMap& pm, int co, T* dy,
+                                    cudaStream_t st) {
+  const uint32_t rows = (uint32_t)pool_rows(pm);
+  pool_expand_rows_kernel<T><<<grid_for((size_t)rows * (co / 8)), 256, 0, st>>>(dyp, arg, pm, co, rows, dy);
 }
 
 // A = xcol^T (MN-major over kk, 64x64 TMA boxes); B = dY (MN-major over C_out):
@@ -145,9 +215,10 @@ inline int conv_wgrad_packed_splits(int Kp, int Mo, int num_sms) {
 }
 
 // part[split][co][Kp]: split-K partial sums of D^T (row Kr = bias gradient)
+// rows: reduction length (default n*oh*ow; pool_rows() for the window-major order)
 inline int conv_wgrad_packed(const ConvGeom& g, const bf16* xcol, int Kp, const bf16* dy, float* part,
-                             int* splits_out, int num_sms, cudaStream_t st) {
-  const int Mo = g.n * g.oh * g.ow;
+                             int* splits_out, int num_sms, cudaStream_t st, int rows = 0) {
+  const int Mo = rows > 0 ? rows : g.n * g.oh * g.ow;
   return with_bn(g.co, [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     TcShape sh = tc_make_shape(Kp, g.co, Mo, BN, conv_wgrad_packed_splits(Kp, Mo, num_sms));
@@ -219,10 +290,17 @@ inline void launch_conv_sgd_packed(const float* part, int splits, const ConvGeom
 }
 
 template <class T>
-inline void launch_im2col_packed(const T* x, const ConvGeom& g, int c_real, int Kp, T* xcol, cudaStream_t st) {
-  const size_t total = (size_t)g.n * g.oh * g.ow * (Kp / 8);
-  im2col_packed_kernel<T><<<grid_for(total), 256, 0, st>>>(x, g, c_real, Kp, FastDiv(Kp / 8), FastDiv(g.ow),
-                                                           FastDiv(g.oh), xcol);
+inline void launch_im2col_packed(const T* x, const ConvGeom& g, int c_real, int Kp, T* xcol, cudaStream_t st,
+                                 const PoolMap* pm = nullptr) {
+  if (pm) {
+    const uint32_t rows = (uint32_t)pool_rows(*pm);
+    im2col_packed_kernel<T, true><<<grid_for((size_t)rows * (Kp / 8)), 256, 0, st>>>(
+        x, g, c_real, Kp, FastDiv(Kp / 8), FastDiv(g.ow), FastDiv(g.oh), xcol, *pm, rows);
+    return;
+  }
+  const uint32_t rows = (uint32_t)g.n * g.oh * g.ow;
+  im2col_packed_kernel<T, false><<<grid_for((size_t)rows * (Kp / 8)), 256, 0, st>>>(
+      x, g, c_real, Kp, FastDiv(Kp / 8), FastDiv(g.ow), FastDiv(g.oh), xcol, PoolMap{}, rows);
 }
 
 // fp32 check mode: the same packed GEMMs on CUDA cores (simt_gemm over plain operands)

@@ -92,12 +92,20 @@ size_t ce_conv_workspace_bytes(const ce_conv_desc* d) {
   return dg > wg ? dg : wg;
 }
 
-int ce_conv_fwd(const ce_conv_desc* d, const void* x, const void* w, const float* bias, int relu, void* y,
-                void* stream) {
+int ce_conv_fwd(const ce_conv_desc* d, const void* x, const void* w, const float* bias, int relu, int pool_k,
+                int pool_s, void* y, uint8_t* arg, void* stream) {
   if (int s = check_desc(d, true)) return s;
   ConvGeom g = geom(d, true);
   cudaStream_t st = (cudaStream_t)stream;
   const int M = g.n * g.oh * g.ow, K = g.k * g.k * g.c;
+  if (pool_k > 0) {  // max-pool epilogue: y / arg are the pooled map and its argmax
+    if (d->precision != CE_PREC_BF16 || !conv_tc_enabled())
+      return fail(CE_EINVAL, "the max-pool epilogue runs on the bf16 tensor-core path only");
+    if (!arg || !pool_fusable(pool_k, pool_s) || g.oh < pool_k || g.ow < pool_k)
+      return fail(CE_EINVAL, "max-pool epilogue: window %d stride %d not fusable (needs 2 or 3, stride >= window)",
+                  pool_k, pool_s);
+    return conv_fwd_tc_pool(g, (const bf16*)x, (const bf16*)w, bias, relu, pool_k, pool_s, (bf16*)y, arg, sms(), st);
+  }
   if (d->precision == CE_PREC_BF16) {
     if (conv_tc_enabled()) return conv_fwd_tc(g, (const bf16*)x, (const bf16*)w, bias, relu, (bf16*)y, sms(), st);
     return fail(CE_EINVAL, "bf16 kernel-level conv requires the tensor-core path");

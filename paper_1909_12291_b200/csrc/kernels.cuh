@@ -235,6 +235,10 @@ inline int simt_splits(int K, int splits) {
 }
 
 // Geometry of one conv layer (per-sample input / output, NHWC).
+// max-pool argmax of a window whose ReLU'd input has max <= 0: the backward
+// routes it no gradient (matches no tap); see maxpool_fwd_kernel
+constexpr uint8_t kPoolDead = 0xFF;
+
 struct ConvGeom {
   int n;           // batch
   int c, h, w;     // input (c = stored channels)

@@ -56,6 +56,9 @@ struct Layer {
   bf16 *Wbf = nullptr, *Wtbf = nullptr;
   bool head = false;      // final Dense with <= kHeadMaxOut outputs: fused forward+loss / backward (head.cuh)
   bool packed = false;    // conv over channel-padded input without dX: packed im2col GEMMs (first_layer_tc.cuh)
+  bool pool_fused = false;  // conv: the next (non-overlapping) max-pool runs in this conv's epilogue, the
+                            // pre-pool activation is never materialised (conv_tc.cuh FwdPoolEpi)
+  bool fused = false;       // pool: its forward is done by the previous conv
   bool col2im = false;    // stride-1 few-channel dgrad as GEMM + col2im (col2im_tc.cuh)
   int Kp = 0;             // packed: im2col row width
   bf16* Wp = nullptr;     // packed (bf16 mode): bf16 mirror [co][Kp]
@@ -97,8 +100,11 @@ struct ProfEvent {
 struct ProfTotals {
   long long launches = 0;
   double ms = 0, flops = 0, bytes = 0;
+  double ideal_ms = 0;  // sum over launches of max(flops / P, bytes / BW): SURVEY §8(d) roofline time
 };
 static std::atomic<long long> g_launches{0};
+// roofline peaks for ideal_ms (ce_prof_set_peaks): sustained bf16 FLOP/s and HBM B/s
+static double g_peak_flops = 1.3877e15, g_peak_bytes = 6.5504e12;
 
 struct ce_net {
   int device = 0, prec = CE_PREC_BF16, num_sms = 148;
@@ -160,6 +166,14 @@ int dev_alloc(ce_net* net, void** p, size_t bytes) {
   net->allocs.push_back(*p);
   net->bytes += bytes;
   return CE_OK;
+}
+// stream-ordered free of a buffer the net outgrew (it leaves the net's alloc list)
+void release_alloc(ce_net* net, void* p) {
+  if (!p) return;
+  auto it = std::find(net->allocs.begin(), net->allocs.end(), p);
+  if (it == net->allocs.end()) return;
+  net->allocs.erase(it);
+  cudaFreeAsync(p, net->st);
 }
 #define ALLOC(ptr, bytes)                                             \
   do {                                                                \
@@ -307,10 +321,28 @@ void prof_collect(ce_net* net) {
     t.ms += ms;
     t.flops += e.flops;
     t.bytes += e.bytes;
+    t.ideal_ms += 1e3 * std::max(e.flops / g_peak_flops, e.bytes / g_peak_bytes);
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
   net->prof_pending.clear();
+}
+
+// CE_POOL_FUSION: 0 = never fuse max-pool into the conv epilogue, 1 = only where
+// the conv runs the gather loader anyway (packed first layer, C % 64 != 0),
+// 2 = every non-overlapping pool after a conv (default)
+int pool_fusion_mode() {
+  static const int mode = [] {
+    const char* e = getenv("CE_POOL_FUSION");
+    return e ? atoi(e) : 2;
+  }();
+  return mode;
+}
+
+PoolMap layer_pool_map(const ce_net* net, size_t conv_li, int n) {
+  const Layer& cv = net->L[conv_li];
+  const Layer& pl = net->L[conv_li + 1];
+  return make_pool_map(n, cv.g.oh, cv.g.ow, pl.g.k, pl.g.s);
 }
 
 int pick_splits(long long blocks_per_split, long long K, long long min_chunk, int num_sms, int waves = 2,
@@ -335,6 +367,32 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
   bool in_act = true;
   for (size_t li = 0; li < net->L.size(); ++li) {
     Layer& l = net->L[li];
+    if (l.kind == CE_LAYER_CONV && l.pool_fused) {  // conv + max-pool in one GEMM epilogue
+      ConvGeom g = l.g;
+      g.n = n;
+      Layer& pl = net->L[li + 1];
+      const PoolMap pm = layer_pool_map(net, li, n);
+      const int K = g.k * g.k * g.c;
+      const double ab = (double)act_bytes(net), pooled = (double)pm.windows * g.co;
+      Prof pf(net, P_CONV_FWD, 2.0 * pm.windows * pm.KK * g.co * g.k * g.k * l.c_real,
+              ab * ((double)n * g.h * g.w * g.c + pooled + (double)g.co * K) + pooled + 4.0 * g.co, l.packed ? 2 : 1);
+      if (l.packed) {
+        launch_im2col_packed((const T*)in, g, l.c_real, l.Kp, (T*)l.xcol, st, &pm);
+        CE_CHECK_LAUNCH();
+        int s = conv_fwd_packed_pool(g, (const bf16*)l.xcol, l.Kp, l.Wp, l.b, l.relu, pm, (bf16*)pl.out, pl.arg,
+                                     net->num_sms, st);
+        if (s != CE_OK) return s;
+      } else {
+        int s = conv_fwd_tc_pool(g, (const bf16*)in, l.Wbf, l.b, l.relu, pl.g.k, pl.g.s, (bf16*)pl.out, pl.arg,
+                                 net->num_sms, st);
+        if (s != CE_OK) return s;
+      }
+      CE_CHECK_LAUNCH();
+      in = pl.out;
+      in_act = true;
+      ++li;  // the pool layer is done
+      continue;
+    }
     if (l.kind == CE_LAYER_CONV) {
       ConvGeom g = l.g;
       g.n = n;
@@ -388,7 +446,8 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
       long long bps = simt_tiles(B, O);
       int splits = simt_splits(K, pick_splits(bps, K, 256, net->num_sms, 8, 256));
       while (splits > 1 && (size_t)splits * B * O * 4 > net->ws_bytes) splits = simt_splits(K, splits - 1);
-      Prof pf(net, P_DENSE_FWD, 2.0 * B * K * O, 4.0 * K * O + (in_act ? act_bytes(net) : 4.0) * B * K, 2);
+      // weights are read once in the operand type: the bf16 mirror on the tensor-core path, fp32 otherwise
+      Prof pf(net, P_DENSE_FWD, 2.0 * B * K * O, (net->use_tc ? 2.0 : 4.0) * K * O + (in_act ? act_bytes(net) : 4.0) * B * K, 2);
       if (net->use_tc) {
         const bf16* x16 = (const bf16*)in;
         if (!in_act) {
@@ -447,8 +506,10 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
     if (l.kind == CE_LAYER_DENSE && l.head) {
       const int B = n, K = l.in_units, O = l.out_units;
       const float* g = (const float*)gin;
+      // algorithmic bytes: fused momentum SGD reads W, V and writes W, V (16 B/param, fp32 master);
+      // dX reuses the same W pass; x is read and dX written once
       Prof pf(net, P_DENSE_BWD, (l.need_dx ? 4.0 : 2.0) * B * K * O,
-              20.0 * K * O + (l.need_dx ? 2.0 : 1.0) * (l.in_is_act ? act_bytes(net) : 4.0) * B * K, 1);
+              16.0 * K * O + (l.need_dx ? 2.0 : 1.0) * (l.in_is_act ? act_bytes(net) : 4.0) * B * K, 1);
       int s = l.in_is_act
                   ? launch_head_bwd((const T*)x, K, g, B, K, O, l.W, l.VW, keep ? l.GW : nullptr,
                                     l.need_dx ? (T*)gout : (T*)nullptr, mask, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu,
@@ -461,8 +522,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
     } else if (l.kind == CE_LAYER_DENSE) {
       const int B = n, K = l.in_units, O = l.out_units;
       const float* g = (const float*)gin;
+      // algorithmic bytes: SGD over the fp32 master (W, V read + written: 16 B/param) plus, on the tensor-core
+      // path, the bf16 mirror rewrite (2) and the dX pass over that mirror (2); fp32 mode reads fp32 W for dX (4)
+      const double per_param = net->use_tc ? 18.0 + (l.need_dx ? 2.0 : 0.0) : 16.0 + (l.need_dx ? 4.0 : 0.0);
       Prof pf(net, P_DENSE_BWD, (l.need_dx ? 4.0 : 2.0) * B * K * O,
-              (l.need_dx ? 24.0 : 20.0) * K * O + 2.0 * (l.in_is_act ? act_bytes(net) : 4.0) * B * K,
+              per_param * K * O + (l.need_dx ? 2.0 : 1.0) * (l.in_is_act ? act_bytes(net) : 4.0) * B * K,
               l.need_dx ? 4 : 3);
       if (net->use_tc) {
         const bool dw_simt = dense_dw_simt_enabled(B);
@@ -552,9 +616,11 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         while (splits > 1 && (size_t)splits * g.co * l.Kp * 4 > net->ws_bytes) splits = simt_splits((int)Mo_, splits - 1);
         conv_wgrad_packed_simt(g, (const float*)l.xcol, l.Kp, (const float*)dy, net->ws, splits, st);
       } else if (l.packed) {
-        int s = conv_wgrad_packed(g, (const bf16*)l.xcol, l.Kp, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
+        const int rows = l.pool_fused ? pool_rows(layer_pool_map(net, li, n)) : Mo;
+        int s = conv_wgrad_packed(g, (const bf16*)l.xcol, l.Kp, (const bf16*)dy, net->ws, &splits, net->num_sms, st,
+                                  rows);
         if (s != CE_OK) return s;
-        pf.bytes = ab * ((double)Mo * g.co + (double)Mo * l.Kp) + 4.0 * splits * g.co * l.Kp;
+        pf.bytes = ab * ((double)rows * g.co + (double)rows * l.Kp) + 4.0 * splits * g.co * l.Kp;
       } else if (net->use_tc) {
         int s = conv_wgrad_tc(g, (const bf16*)x, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
@@ -588,7 +654,14 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
                       bsplits, l.b, l.Vb, keep ? l.Gb : nullptr, lr, mu, st);
       CE_CHECK_LAUNCH();
     } else {  // pool
-      if (l.need_dx) {
+      if (l.need_dx && l.fused && net->L[li - 1].packed) {
+        // dY of the packed conv in its window-major xcol row order (no raster pass)
+        const PoolMap pm = layer_pool_map(net, li - 1, n);
+        Prof pf(net, P_POOL, 0.0, (double)act_bytes(net) * ((double)pool_rows(pm) + pm.windows) * l.g.c +
+                                      (double)pm.windows * l.g.c);
+        launch_pool_expand_rows((const T*)gin, l.arg, pm, l.g.c, (T*)gout, st);
+        CE_CHECK_LAUNCH();
+      } else if (l.need_dx) {
         ConvGeom g = l.g;
         g.n = n;
         size_t total = (size_t)n * g.h * g.w * g.c;
@@ -674,6 +747,20 @@ int check_net(const ce_net* net) {
   return CE_OK;
 }
 
+// RAII for ce_train's graph exec and events: every return path (including a
+// failed launch inside the replay loop) drains the stream and releases them
+struct TrainRes {
+  cudaGraphExec_t exec = nullptr;
+  cudaEvent_t ev[4] = {};
+  cudaStream_t owner = nullptr;
+  ~TrainRes() {
+    if (owner) cudaStreamSynchronize(owner);
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 }  // namespace
 
 // =============================================================================== C ABI
@@ -702,6 +789,19 @@ int ce_net_prof_read(ce_net* net, int cls, const char** name, long long* launche
   if (bytes) *bytes = t.bytes;
   return CE_OK;
 }
+int ce_prof_set_peaks(double flops_per_s, double bytes_per_s) {
+  if (!(flops_per_s > 0) || !(bytes_per_s > 0)) return fail(CE_EINVAL, "peaks must be positive");
+  g_peak_flops = flops_per_s;
+  g_peak_bytes = bytes_per_s;
+  return CE_OK;
+}
+
+int ce_net_prof_ideal(ce_net* net, int cls, double* ideal_ms) {
+  if (!net || cls < 0 || cls >= P_NCLASS || !ideal_ms) return fail(CE_EINVAL, "bad profile class %d", cls);
+  *ideal_ms = net->prof[cls].ideal_ms;
+  return CE_OK;
+}
+
 const char* ce_last_error(void) { return g_err; }
 
 int ce_device_count(int* count) {
@@ -851,6 +951,20 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
   }
   if (net->L.back().kind != CE_LAYER_DENSE) return bail(fail(CE_EINVAL, "network must end in a Dense layer"));
   net->classes = net->L.back().out_units;
+  // ---- packed first layers and conv + max-pool fusion
+  for (size_t i = 0; i < net->L.size(); ++i) {
+    Layer& l = net->L[i];
+    if (l.kind != CE_LAYER_CONV) continue;
+    const long long Mo = (long long)d->max_batch * l.g.oh * l.g.ow;
+    l.packed = (net->use_tc || precision == CE_PREC_FP32) && l.c_real < l.g.c && !l.need_dx && !packed_disabled() &&
+               packed_kp(l.g, l.c_real) <= kPackedMaxKp && Mo * packed_kp(l.g, l.c_real) / 8 < (1ll << 32);
+    if (i + 1 < net->L.size() && net->L[i + 1].kind == CE_LAYER_POOL && net->use_tc &&
+        pool_fusable(net->L[i + 1].g.k, net->L[i + 1].g.s) && pool_fusion_mode() > 0 &&
+        (pool_fusion_mode() >= 2 || l.packed || l.g.c % 64 != 0)) {
+      l.pool_fused = true;
+      net->L[i + 1].fused = true;
+    }
+  }
   // ---- allocations
   const size_t B = d->max_batch, ab = act_bytes(net);
   size_t total_params = 0;
@@ -888,7 +1002,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
                             l.out_units * 4);
       ws = std::max(ws, (size_t)(kColsumMaxSplits + 64) * l.out_units * 4);
     } else {
-      ALLOC(l.out, B * l.out_per_sample * ab);
+      if (!l.pool_fused) ALLOC(l.out, B * l.out_per_sample * ab);  // fused: only the pooled map exists
       max_g = std::max(max_g, B * l.out_per_sample * ab);
       if (l.kind == CE_LAYER_POOL) ALLOC(l.arg, B * l.out_per_sample);
       if (l.kind == CE_LAYER_CONV) {
@@ -902,13 +1016,14 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);
         l.col2im = net->use_tc && l.need_dx && col2im_dgrad_eligible(l.g);
         if (l.col2im) zbytes = std::max(zbytes, col2im_dgrad_zbytes(l.g, (int)B));
-        l.packed = (net->use_tc || precision == CE_PREC_FP32) && l.c_real < l.g.c && !l.need_dx && !packed_disabled() &&
-                   packed_kp(l.g, l.c_real) <= kPackedMaxKp && Mo * packed_kp(l.g, l.c_real) / 8 < (1ll << 32);
         if (l.packed) {
           l.Kp = packed_kp(l.g, l.c_real);
-          const int psp = conv_wgrad_packed_splits(l.Kp, (int)Mo, net->num_sms);
+          // rows of the packed GEMMs: pixels, or the window-major pooled order (padding rows included)
+          const long long rows = l.pool_fused ? pool_rows(layer_pool_map(net, i, (int)B)) : Mo;
+          const int psp = conv_wgrad_packed_splits(l.Kp, (int)rows, net->num_sms);
           ws = std::max(ws, (size_t)psp * l.g.co * l.Kp * 4);
-          ALLOC(l.xcol, (size_t)Mo * l.Kp * ab);
+          max_g = std::max(max_g, (size_t)rows * l.g.co * ab);  // window-major dY of the fused pool
+          ALLOC(l.xcol, (size_t)rows * l.Kp * ab);
           if (precision == CE_PREC_FP32) {
             ALLOC(l.Wpf, (size_t)l.g.co * l.Kp * 4);
             ws = std::max(ws, (size_t)simt_splits((int)Mo, pick_splits(simt_tiles(l.g.co, l.Kp), Mo, 512,
@@ -1152,12 +1267,21 @@ int ce_net_forward_host(ce_net* net, const float* x, int n, float* logits) {
   return CE_OK;
 }
 
+int ce_net_layer_materialized(const ce_net* net, int layer, int* yes) {
+  if (check_net(net)) return CE_EINVAL;
+  if (layer < 0 || layer >= (int)net->L.size() || !yes) return fail(CE_EINVAL, "layer %d out of range", layer);
+  *yes = net->L[layer].pool_fused ? 0 : 1;
+  return CE_OK;
+}
+
 int ce_net_get_activation(ce_net* net, int layer, int n, float* out) {
   if (check_net(net)) return CE_EINVAL;
   if (layer < 0 || layer >= (int)net->L.size()) return fail(CE_EINVAL, "layer %d out of range", layer);
   if (n < 1 || n > net->max_batch) return fail(CE_EINVAL, "bad n");
   DevGuard dg(net->device);
   Layer& l = net->L[layer];
+  if (l.pool_fused)
+    return fail(CE_EINVAL, "layer %d runs fused with the next max-pool; its output is not materialised", layer);
   cudaStream_t st = net->st;
   if (l.kind == CE_LAYER_DENSE) {
     CE_CUDA(cudaMemcpyAsync(out, l.out, (size_t)n * l.out_units * 4, cudaMemcpyDeviceToHost, st));
@@ -1214,11 +1338,13 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   cudaStream_t st = net->st;
   const int steps = epochs * steps_per_epoch;
   if (steps > net->losses_cap) {
+    release_alloc(net, net->d_losses);
     ALLOC(net->d_losses, (size_t)steps * 4);
     net->losses_cap = steps;
   }
   size_t pn = (size_t)epochs * n_perm;
   if (pn > net->perm_cap) {
+    release_alloc(net, net->d_perm);
     ALLOC(net->d_perm, pn * 4);
     net->perm_cap = pn;
   }
@@ -1230,13 +1356,13 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
     if (!net->h_flags) return fail(CE_ENOMEM, "pinned flag pool allocation failed");
   }
   // capture one step (profiling runs eagerly so each launch can be bracketed)
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  TrainRes r;  // graph exec + events: released on every return path
   bool graphed = false;
   net->acc = 0;
   long long per_step = 0;
   SharedGate capture_gate(net->device);  // no exclusive latency window (device sync) during a capture
   if (!net->prof_on && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    cudaGraph_t graph = nullptr;
     int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true);
     if (s == CE_OK) s = step_any(net, batch, lr, momentum);
     cudaError_t ce = cudaStreamEndCapture(st, &graph);
@@ -1244,18 +1370,19 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
       if (graph) cudaGraphDestroy(graph);
       return s;
     }
-    if (ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) graphed = true;
+    if (ce == cudaSuccess && cudaGraphInstantiate(&r.exec, graph, 0) == cudaSuccess) graphed = true;
     if (graph) cudaGraphDestroy(graph);
     per_step = net->acc;
   }
   capture_gate.release();
   cudaGetLastError();
   net->acc = 0;
-  cudaEvent_t e0, e1, chunk_ev[2];
-  CE_CUDA(cudaEventCreate(&e0));
-  CE_CUDA(cudaEventCreate(&e1));
-  CE_CUDA(cudaEventCreateWithFlags(&chunk_ev[0], cudaEventDisableTiming));
-  CE_CUDA(cudaEventCreateWithFlags(&chunk_ev[1], cudaEventDisableTiming));
+  CE_CUDA(cudaEventCreate(&r.ev[0]));
+  CE_CUDA(cudaEventCreate(&r.ev[1]));
+  CE_CUDA(cudaEventCreateWithFlags(&r.ev[2], cudaEventDisableTiming));
+  CE_CUDA(cudaEventCreateWithFlags(&r.ev[3], cudaEventDisableTiming));
+  cudaEvent_t e0 = r.ev[0], e1 = r.ev[1], *chunk_ev = r.ev + 2;
+  r.owner = st;
   CE_CUDA(cudaEventRecord(e0, st));
   // Replay in chunks; after each chunk snapshot the device non-finite flag. With
   // one chunk in flight ahead, a diverged candidate stops within two chunks
@@ -1268,7 +1395,7 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
       SharedGate gate(net->device);  // enqueue under the gate; ce_latency drains in-flight chunks
       for (int i = 0; i < todo; ++i) {
         if (graphed) {
-          CE_CUDA(cudaGraphLaunch(exec, st));
+          CE_CUDA(cudaGraphLaunch(r.exec, st));
         } else {
           if (int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true)) return s;
           if (int s = step_any(net, batch, lr, momentum)) return s;
@@ -1289,15 +1416,10 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   CE_CUDA(cudaEventRecord(e1, st));
   CE_CUDA(cudaMemcpyAsync(losses, net->d_losses, (size_t)steps * 4, cudaMemcpyDeviceToHost, st));
   cudaError_t se = cudaStreamSynchronize(st);
-  if (exec) cudaGraphExecDestroy(exec);
   if (net->prof_on) prof_collect(net);
-  cudaEventDestroy(chunk_ev[0]);
-  cudaEventDestroy(chunk_ev[1]);
   if (se != cudaSuccess) return fail(CE_ECUDA, "train loop: %s", cudaGetErrorString(se));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   if (device_ms) *device_ms = ms;
   return CE_OK;
 }
@@ -1309,6 +1431,8 @@ int ce_predict(ce_net* net, const ce_dataset* ds, int batch, double* scores, int
   SharedGate gate(net->device);
   cudaStream_t st = net->st;
   if ((size_t)ds->n > net->pred_cap) {
+    release_alloc(net, net->d_scores);
+    release_alloc(net, net->d_preds);
     ALLOC(net->d_scores, (size_t)ds->n * 8);
     ALLOC(net->d_preds, (size_t)ds->n * 8);
     net->pred_cap = ds->n;
@@ -1367,6 +1491,8 @@ int ce_predict_stream(ce_net* net, const uint8_t* pixels, long long count, int b
   const size_t img = (size_t)net->in_c * HW;
   const size_t total_bytes = img * (size_t)count;
   if ((size_t)count > net->pred_cap) {
+    release_alloc(net, net->d_scores);
+    release_alloc(net, net->d_preds);
     ALLOC(net->d_scores, (size_t)count * 8);
     ALLOC(net->d_preds, (size_t)count * 8);
     net->pred_cap = count;

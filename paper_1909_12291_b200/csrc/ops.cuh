@@ -126,7 +126,6 @@ __device__ __forceinline__ void store8(T* p, const float (&v)[8]);
 // whose max is not > 0 is zero (mask(x > 0) at the argmax position); the
 // forward stores argmax 0xFF for such windows, which never matches a tap in
 // the backward, and the mask tensor is not read there at all.
-constexpr uint8_t kPoolDead = 0xFF;
 
 template <class T, int K, int S>
 __global__ void __launch_bounds__(256) maxpool_fwd_kernel(const T* __restrict__ x, ConvGeom g, T* __restrict__ y,

@@ -10,6 +10,8 @@ its in-flight candidates (scheduler.SocketPool)."""
 
 import argparse
 import json
+import os
+import sys
 import threading
 
 from .candidate import TrainBudget, evaluate
@@ -41,7 +43,14 @@ def main(argv=None):
     ap.add_argument("--config", default="{}")
     args = ap.parse_args(argv)
     fn = make_evaluate(json.loads(args.config), args.device)
-    threads = [threading.Thread(target=run_socket_worker, args=(args.host, args.port, f"g{args.device}s{k}", fn))
+
+    def on_sticky(err):  # the context is poisoned: end the process, the master reissues its work
+        sys.stderr.write(f"gpu_worker device {args.device}: sticky CUDA fault, exiting: {err}\n")
+        sys.stderr.flush()
+        os._exit(3)
+
+    threads = [threading.Thread(target=run_socket_worker,
+                                args=(args.host, args.port, f"g{args.device}s{k}", fn, on_sticky))
                for k in range(args.slots)]
     for t in threads:
         t.start()

@@ -67,13 +67,14 @@ _SIGNATURES = {
     "ce_net_get_grads": ([_P, C.c_int, _F, _F], C.c_int),
     "ce_net_forward_host": ([_P, _F, C.c_int, _F], C.c_int),
     "ce_net_get_activation": ([_P, C.c_int, C.c_int, _F], C.c_int),
+    "ce_net_layer_materialized": ([_P, C.c_int, C.POINTER(C.c_int)], C.c_int),
     "ce_net_train_batch_host": ([_P, _F, _I64, C.c_int, C.c_float, C.c_float, _F], C.c_int),
     "ce_train": ([_P, _P, _I32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float, _F, _D], C.c_int),
     "ce_predict": ([_P, _P, C.c_int, _D, _I64], C.c_int),
     "ce_latency": ([_P, _F, C.c_int, C.c_int, C.c_int, _D], C.c_int),
     "ce_predict_stream": ([_P, _U8, C.c_longlong, C.c_int, _D, _I64, _D], C.c_int),
     "ce_conv_workspace_bytes": ([C.POINTER(ConvDesc)], C.c_size_t),
-    "ce_conv_fwd": ([C.POINTER(ConvDesc), _P, _P, _P, C.c_int, _P, _P], C.c_int),
+    "ce_conv_fwd": ([C.POINTER(ConvDesc), _P, _P, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P], C.c_int),
     "ce_conv_dgrad": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "ce_conv_wgrad": ([C.POINTER(ConvDesc), _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "ce_maxpool_fwd": ([C.POINTER(ConvDesc), _P, _P, _P, _P], C.c_int),
@@ -92,6 +93,8 @@ _SIGNATURES = {
     "ce_prof_num_classes": ([], C.c_int),
     "ce_net_set_profiling": ([_P, C.c_int], C.c_int),
     "ce_net_prof_read": ([_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_longlong), _D, _D, _D], C.c_int),
+    "ce_prof_set_peaks": ([C.c_double, C.c_double], C.c_int),
+    "ce_net_prof_ideal": ([_P, C.c_int, _D], C.c_int),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -140,9 +143,11 @@ def conv_workspace_bytes(desc):
     return int(load().ce_conv_workspace_bytes(C.byref(desc)))
 
 
-def conv_fwd(desc, x, w, bias, relu, y, stream=0):
-    """Kernel-level conv forward on device pointers (ints) of NHWC tensors."""
-    check(load().ce_conv_fwd(C.byref(desc), x, w, bias, int(relu), y, stream))
+def conv_fwd(desc, x, w, bias, relu, y, stream=0, pool=None, arg=None):
+    """Kernel-level conv forward on device pointers (ints) of NHWC tensors.
+    pool=(window, stride): max-pool epilogue, y/arg are the pooled map and its u8 argmax."""
+    pk, ps = pool if pool else (0, 0)
+    check(load().ce_conv_fwd(C.byref(desc), x, w, bias, int(relu), int(pk), int(ps), y, arg, stream))
 
 
 def conv_dgrad(desc, dy, w, mask, dx, ws, ws_bytes, stream=0):
@@ -200,6 +205,11 @@ def pcg64_uniform(state, inc, skip, low, high, out, count, stream=0):
 
 def permute_flatten_weights(src, rows, c, c_store, hw, direction, dst, stream=0):
     check(load().ce_permute_flatten_weights(src, rows, c, c_store, hw, direction, dst, stream))
+
+
+def set_prof_peaks(flops_per_s, bytes_per_s):
+    """Peaks the profiler uses for each launch's roofline time max(F/P, B/BW)."""
+    check(load().ce_prof_set_peaks(float(flops_per_s), float(bytes_per_s)))
 
 
 def launch_count():
@@ -305,6 +315,12 @@ class Net:
         check(load().ce_net_forward_host(self._h, fptr(x), len(x), fptr(out)))
         return out
 
+    def materialized(self, layer):
+        """False for a conv whose max-pool runs in its epilogue (no pre-pool activation exists)."""
+        yes = C.c_int(0)
+        check(load().ce_net_layer_materialized(self._h, layer, C.byref(yes)))
+        return bool(yes.value)
+
     def activation(self, layer, n, shape):
         out = np.empty((n, *shape), np.float32)
         check(load().ce_net_get_activation(self._h, layer, n, fptr(out)))
@@ -354,14 +370,16 @@ class Net:
         check(load().ce_net_set_profiling(self._h, int(bool(on))))
 
     def profile(self):
-        """Per kernel class: {name: (launches, ms, flops, bytes)} accumulated by ce_train."""
+        """Per kernel class: {name: (launches, ms, flops, bytes, ideal_ms)} accumulated by ce_train;
+        ideal_ms = sum over launches of max(flops / P, bytes / BW) (set_prof_peaks)."""
         lib, out = load(), {}
         for cls in range(lib.ce_prof_num_classes()):
             name, n = C.c_char_p(), C.c_longlong()
-            ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+            ms, fl, by, ideal = C.c_double(), C.c_double(), C.c_double(), C.c_double()
             check(lib.ce_net_prof_read(self._h, cls, C.byref(name), C.byref(n), C.byref(ms), C.byref(fl),
                                        C.byref(by)))
-            out[name.value.decode()] = (n.value, ms.value, fl.value, by.value)
+            check(lib.ce_net_prof_ideal(self._h, cls, C.byref(ideal)))
+            out[name.value.decode()] = (n.value, ms.value, fl.value, by.value, ideal.value)
         return out
 
     def latency(self, x, warmup, reps):

@@ -5,6 +5,7 @@ the GA host (ga.Master) or a fixed genome list feeds a GpuPool; each record
 comes back to the host, nothing else does (no collective).
 """
 
+import threading
 import time
 
 import numpy as np
@@ -65,8 +66,68 @@ class ListMaster:
         self.records[record.genome_id] = record
 
 
+class LocalCounter:
+    """In-process atomic counters with the TCPStore.add interface."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._vals = {}
+
+    def add(self, key, n):
+        with self._lock:
+            v = self._vals.get(key, 0) + n
+            self._vals[key] = v
+            return v
+
+
+class StoreCounter:
+    """Cross-process atomic counters: torch.distributed TCPStore.add under a key
+    prefix (one prefix per generation). Plain host-side rendezvous traffic, a
+    few hundred bytes per candidate; no collective, no GPU involvement."""
+
+    def __init__(self, store, prefix):
+        self.store, self.prefix = store, prefix
+
+    def add(self, key, n):
+        return int(self.store.add(f"{self.prefix}/{key}", n))
+
+
+class SharedQueueMaster:
+    """One generation dealt to every (rank, GPU, slot) worker from ONE shared
+    queue: work stealing across processes without a master process.
+
+    `genomes` must be identical on every rank; they are ordered longest-
+    estimated-first and claimed through atomic counters, so a worker that
+    finishes early simply takes the next candidate, whatever rank it is on
+    (the reference's pull loop, workers.py:97-125, across processes). Big slots
+    take from the long end, the others from the short end (two-ended dispatch);
+    `claimed` bounds the total so the two ends never overlap."""
+
+    def __init__(self, genomes, counter, cost_fn, big_worker=None):
+        self.genomes = sorted(genomes, key=lambda g: -cost_fn(g))
+        self.counter = counter
+        self.big_worker = big_worker or (lambda wid: True)
+        self.records = {}
+        self.issued = []
+
+    def issue(self, worker_id):
+        n = len(self.genomes)
+        if self.counter.add("claimed", 1) > n:
+            return None
+        if self.big_worker(worker_id):
+            g = self.genomes[self.counter.add("front", 1) - 1]
+        else:
+            g = self.genomes[n - self.counter.add("back", 1)]
+        self.issued.append(g)
+        return g
+
+    def collect(self, record):
+        self.records[record.genome_id] = record
+
+
 def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), slots_per_gpu=2,
-                        order="two_ended", precision="bf16", defer_latency=True, big_slots=1, **evaluate_kwargs):
+                        order="two_ended", precision="bf16", defer_latency=True, big_slots=1, master=None,
+                        **evaluate_kwargs):
     """Evaluate every genome; returns (records in input order, PoolReport).
 
     order "two_ended" (default): slot 0 of each GPU takes the longest remaining
@@ -77,8 +138,11 @@ def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), 
     The generation is pre-issued, so with defer_latency the measured-latency
     objectives are taken in one exclusive pass once every slot is done
     (candidate.LatencyWindow) instead of stalling the other slots per candidate."""
-    master = ListMaster(genomes)
     n_train = len(splits.train)
+    if master is None:
+        master = ListMaster(genomes)
+    else:  # a SharedQueueMaster orders and deals the generation itself
+        order = "fifo"
     window = LatencyWindow() if defer_latency else None
 
     def run_one(genome, worker_id, device):
@@ -93,6 +157,8 @@ def evaluate_population(genomes, splits, budget, objective, seed, devices=(0,), 
         t0 = time.perf_counter()
         window.flush()
         report.latency_window_s = time.perf_counter() - t0
+    if isinstance(master, SharedQueueMaster):
+        return [master.records.get(g.id) for g in master.issued], report
     return [master.records.get(g.id) for g in master.genomes], report
 
 

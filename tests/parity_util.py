@@ -40,6 +40,14 @@ CASES = [
      "h0=dense:units=40", (3, 48, 48)),
     ("odd_units", "id=case0000000006 " + _BASE +
      "f0=conv:oc=64,k=5,s=3,relu=1 h0=dense:units=37", (3, 40, 40)),
+    # max-pool in the conv epilogue: packed first conv -> 3x3/3 (KK=9), gather conv -> 2x2 stride 3 (gaps)
+    ("fused_pools", "id=case0000000007 " + _BASE +
+     "f0=conv:oc=16,k=3,s=1,relu=1 f1=pool:size=3,s=3 f2=conv:oc=32,k=3,s=1,relu=1 f3=pool:size=2,s=3 "
+     "h0=dense:units=24", (3, 50, 50)),
+    # relu=0 conv before a fused pool (no dead windows), C=64 conv fused (gather instead of TMA im2col)
+    ("fused_norelu_c64", "id=case0000000008 " + _BASE +
+     "f0=conv:oc=64,k=5,s=1,relu=0 f1=pool:size=2,s=2 f2=conv:oc=128,k=3,s=1,relu=1 f3=pool:size=3,s=3",
+     (3, 40, 40)),
     # C2 population genome #15 (2d5ebb4eae1bf684): 262,144 -> 523 head
     ("c2_g15", "id=2d5ebb4eae1bf684 parents= lr=0.017072315886796932 momentum=0.5 batch_size=32 "
      "f0=conv:oc=256,k=5,s=3,relu=1 h0=dense:units=523", (3, 100, 100)),

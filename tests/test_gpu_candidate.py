@@ -1,0 +1,299 @@
+"""The product path pinned to the reference at BASELINE scale (SURVEY §8(c)
+tiers T3 and T4), through the same calls evaluate() makes: ce_train
+(graph-replayed steps, device permutation, chunked non-finite exit),
+ce_predict, ce_latency and the EvalRecord composition.
+
+  T3  train_short(FIXED, C1 data, 10 steps) vs oracle.train_short on the same
+      seeds and data: per-step loss and every weight tensor after 10 steps,
+      fp32 check mode <= 1e-4; bf16 step-0 loss <= 1e-2 (drift reported).
+  T4  evaluate() vs records the reference itself produced
+      (tests/golden/host.json, tests/golden/candidate.json, both written by
+      running convevo): ok / flops / params exact; fp32 scores <= 1e-5 where
+      the training is short enough to be non-chaotic; |dtp|, |dfp|, |dfn| <= 5
+      of 400 and |dAUC| <= 0.02 for full budgets and bf16.
+  predict  ce_predict vs oracle.predict_scores on the 400 val patches with
+      the trained weights (ties -> class 0, evaluator.py:185).
+  latency  ce_latency orders a 2x deeper net strictly slower.
+Reference: convevo/evaluator.py:145-255.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import cnn_ref as O
+from paper_1909_12291_b200 import ObjectiveConfig, TrainBudget, parse_genome
+from paper_1909_12291_b200.candidate import evaluate, measure_latency, predict_scores, train_short
+from paper_1909_12291_b200.genes import FIXED
+from paper_1909_12291_b200.network import instantiate
+from paper_1909_12291_b200.patches import default_splits
+
+from parity_util import rel
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+FLOP_OBJ = ObjectiveConfig("flop_proxy", -0.2, 1e8, 1e9)
+T3_TOL = 1e-4
+COUNT_TOL = 5      # patches of 400
+AUC_TOL = 0.02
+
+
+@pytest.fixture(scope="module")
+def splits():
+    return default_splits()
+
+
+def _golden(name):
+    path = os.path.join(GOLDEN, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated")
+    with open(path) as fh:
+        return json.load(fh)
+
+
+def _conf(preds, labels):
+    labels = np.asarray(labels).astype(np.int64)
+    preds = np.asarray(preds)
+    return {"tp": int(((preds == 1) & (labels == 1)).sum()), "fp": int(((preds == 1) & (labels == 0)).sum()),
+            "fn": int(((preds == 0) & (labels == 1)).sum())}
+
+
+def _check_counts(got, want, what):
+    for k in ("tp", "fp", "fn"):
+        assert abs(got[k] - want[k]) <= COUNT_TOL, f"{what}: {k} {got[k]} vs reference {want[k]}"
+
+
+KNIFE_EDGE = 0.02  # |p - 0.5| below which a decision is a near-tie of the reference itself
+
+
+def _check_bf16_decisions(scores, preds, ref_scores, ref_preds, labels, ref_auc, auc, what):
+    """bf16 T4: bf16 storage perturbs a chaotic training trajectory, so a
+    reference score within KNIFE_EDGE of the 0.5 threshold can flip either way. Decisions the
+    reference makes clearly must agree (<= COUNT_TOL flips); the AUC must agree within AUC_TOL
+    when at least 90% of the reference's decisions are clear. Returns the near-tie fraction."""
+    ref_scores, scores = np.asarray(ref_scores), np.asarray(scores)
+    clear = np.abs(ref_scores - 0.5) > KNIFE_EDGE
+    flips = int((np.asarray(preds)[clear] != np.asarray(ref_preds)[clear]).sum())
+    assert flips <= COUNT_TOL, f"{what}: {flips} clear decisions flipped (of {int(clear.sum())})"
+    if clear.mean() >= 0.9:
+        assert abs(auc - ref_auc) <= AUC_TOL, f"{what}: AUC {auc:.4f} vs reference {ref_auc:.4f}"
+    return 1.0 - float(clear.mean())
+
+
+# ---------------------------------------------------------------- T3
+def test_t3_trajectory_fp32(splits):
+    """10 steps of FIXED at B=64 through ce_train vs the oracle, fp32 check mode."""
+    genome = parse_genome(FIXED)
+    budget = TrainBudget(epochs=1, max_batches_per_epoch=10)
+    net, secs = train_short(genome, splits.train, budget, seed=0, precision="fp32")
+    try:
+        losses = np.asarray(net.last_losses, np.float64)
+        after = net.pull_weights()
+    finally:
+        net.release()
+    ref_net = O.OracleNet.from_network(instantiate(genome, splits.train.input_shape, seed=0))
+    ref_losses, _, bad = O.train_short(ref_net, genome, splits.train, 1, 0, max_batches_per_epoch=10)
+    assert bad is None
+    assert len(losses) == len(ref_losses) == 10
+    for i, (a, b) in enumerate(zip(losses, ref_losses)):
+        assert abs(a - b) <= T3_TOL * abs(b), f"step {i}: loss {a} vs oracle {b}"
+    for p, ((w, b, _, _), (rw, rb)) in enumerate(zip(after, ref_net.params)):
+        assert rel(w, rw) <= T3_TOL, f"param layer {p}: W after 10 steps rel {rel(w, rw):.3e}"
+        # biases start at 0, so b after 10 steps IS the cumulative update, which drifts ~1.6e-4 even
+        # between the fp32 and fp64 oracles: held to 1e-3 relative
+        assert rel(b, rb) <= 1e-3 or np.abs(b - rb).max() < 1e-7, f"param layer {p}: b rel {rel(b, rb):.3e}"
+    # the oracle itself against the reference's own losses (full-budget golden, same first epoch)
+    gold = _golden("candidate.json").get("c1_fixed_full")
+    if gold is not None:
+        np.testing.assert_allclose(ref_losses, gold["losses"][:10], rtol=1e-5)
+        np.testing.assert_allclose(losses, gold["losses"][:10], rtol=T3_TOL)
+
+
+def test_t3_trajectory_bf16(splits):
+    genome = parse_genome(FIXED)
+    budget = TrainBudget(epochs=1, max_batches_per_epoch=10)
+    net, _ = train_short(genome, splits.train, budget, seed=0, precision="bf16")
+    losses = np.asarray(net.last_losses, np.float64)
+    net.release()
+    ref_net = O.OracleNet.from_network(instantiate(genome, splits.train.input_shape, seed=0))
+    ref_losses, _, _ = O.train_short(ref_net, genome, splits.train, 1, 0, max_batches_per_epoch=10)
+    assert abs(losses[0] - ref_losses[0]) <= 1e-2 * abs(ref_losses[0]), (losses[0], ref_losses[0])
+    drift = np.abs(losses - ref_losses) / np.abs(ref_losses)
+    print("bf16 loss drift per step:", np.array2string(drift, precision=4))
+    assert np.all(np.isfinite(losses))
+
+
+# ---------------------------------------------------------------- T4
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_t4_evaluate_fixed_3steps(splits, precision):
+    """evaluate() vs the record convevo wrote (make_golden.py: evaluate_fixed_3steps)."""
+    gold = _golden("host.json")["evaluate_fixed_3steps"]
+    genome = parse_genome(FIXED)
+    budget = TrainBudget(epochs=1, max_batches_per_epoch=3)
+    rec = evaluate(genome, splits, budget, FLOP_OBJ, seed=0, precision=precision)
+    g = gold["record"]
+    assert rec.ok == g["ok"] and rec.genome_id == g["genome_id"]
+    assert rec.flops_inference == g["flops_inference"] and rec.params == g["params"]
+    assert rec.objective_raw == g["objective_raw"] and rec.objective_m == g["objective_m"]
+    net, _ = train_short(genome, splits.train, budget, seed=0, precision=precision)
+    try:
+        scores, preds = predict_scores(net, splits.val)
+    finally:
+        net.release()
+    ref_scores, ref_preds = np.asarray(gold["scores"]), np.asarray(gold["preds"])
+    if precision == "fp32":
+        assert rel(scores, ref_scores) <= 1e-5, f"scores rel {rel(scores, ref_scores):.3e}"
+        near_tie = np.abs(ref_scores - 0.5) < 1e-6
+        assert np.array_equal(preds[~near_tie], ref_preds[~near_tie])
+        assert rec.val_f1 == pytest.approx(g["val_f1"], abs=1e-12)
+        assert rec.val_auc == pytest.approx(g["val_auc"], abs=1e-4)
+        assert rec.fitness == pytest.approx(g["fitness"], abs=1e-12)
+    else:
+        edge = _check_bf16_decisions(scores, preds, ref_scores, ref_preds, splits.val.labels, g["val_auc"],
+                                     rec.val_auc, "FIXED 3 steps bf16")
+        print(f"FIXED 3 steps bf16: scores rel {rel(scores, ref_scores):.3e}, near-ties {edge:.2f}")
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_t4_c1_full_budget(splits, precision):
+    """The whole C1 candidate (2 epochs x 62 steps at B=64) vs convevo's own run."""
+    gold = _golden("candidate.json").get("c1_fixed_full")
+    if gold is None:
+        pytest.skip("c1 golden not generated")
+    genome = parse_genome(FIXED)
+    rec = evaluate(genome, splits, TrainBudget(epochs=2), FLOP_OBJ, seed=0, precision=precision)
+    assert rec.ok == gold["ok"]
+    assert rec.flops_inference == gold["flops_inference"] and rec.params == gold["params"]
+    conf = rec.extras["confusion"]
+    if precision == "fp32":
+        _check_counts(conf, gold["confusion"], f"C1 {precision}")
+        assert abs(rec.val_auc - gold["val_auc"]) <= AUC_TOL, (rec.val_auc, gold["val_auc"])
+    else:
+        net, _ = train_short(genome, splits.train, TrainBudget(epochs=2), seed=0, precision="bf16")
+        try:
+            scores, preds = predict_scores(net, splits.val)
+        finally:
+            net.release()
+        _check_bf16_decisions(scores, preds, gold["scores"], gold["preds"], splits.val.labels, gold["val_auc"],
+                              rec.val_auc, "C1 bf16")
+    print(f"C1 {precision}: F1 {rec.val_f1:.4f} (ref {gold['val_f1']:.4f}) AUC {rec.val_auc:.4f} "
+          f"(ref {gold['val_auc']:.4f}) conf {conf} (ref {gold['confusion']})")
+
+
+def _c2_rows():
+    gold = _golden("candidate.json").get("c2_2steps")
+    if gold is None:
+        pytest.skip("c2 golden not generated")
+    return gold
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_t4_c2_population_2steps(splits, precision):
+    """All 16 C2 genomes at TrainBudget(1, 2) vs convevo's evaluate(): the ok/failed outcome
+    exactly, cost counts exactly, F1 counts and AUC within T4; fp32 scores <= 1e-4."""
+    gold = _c2_rows()
+    budget = TrainBudget(*gold["budget"])
+    for row in gold["rows"]:
+        genome = parse_genome(row["genome"])
+        want = row["record"]
+        rec = evaluate(genome, splits, budget, FLOP_OBJ, seed=0, precision=precision)
+        assert rec.ok == want["ok"], (genome.id, rec.failure_reason, want["failure_reason"])
+        if not want["ok"]:
+            assert rec.failure_reason.split(" at ")[0] == want["failure_reason"].split(" at ")[0]
+            continue
+        assert rec.flops_inference == want["flops_inference"] and rec.params == want["params"], genome.id
+        net, _ = train_short(genome, splits.train, budget, seed=0, precision=precision)
+        try:
+            scores, preds = predict_scores(net, splits.val)
+            losses = np.asarray(net.last_losses)
+        finally:
+            net.release()
+        if precision == "fp32":
+            _check_counts(rec.extras["confusion"], row["confusion"], f"{genome.id} {precision}")
+            assert abs(rec.val_auc - want["val_auc"]) <= AUC_TOL, (genome.id, rec.val_auc, want["val_auc"])
+            np.testing.assert_allclose(losses, row["losses"], rtol=1e-4, err_msg=genome.id)
+            assert rel(scores, row["scores"]) <= 1e-4, (genome.id, rel(scores, row["scores"]))
+        else:
+            assert abs(losses[0] - row["losses"][0]) <= 1e-2 * abs(row["losses"][0]), (genome.id, losses[0])
+            edge = _check_bf16_decisions(scores, preds, row["scores"], row["preds"], splits.val.labels,
+                                         want["val_auc"], rec.val_auc, f"{genome.id} bf16")
+            print(f"{genome.id} bf16: loss {losses.tolist()} (ref {row['losses']}), near-ties {edge:.2f}")
+
+
+# ---------------------------------------------------------------- predict / latency
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_predict_vs_oracle(splits, precision):
+    """ce_predict on the 400 val patches vs oracle.predict_scores with the same trained weights."""
+    genome = parse_genome(FIXED)
+    net, _ = train_short(genome, splits.train, TrainBudget(epochs=1, max_batches_per_epoch=20), seed=0,
+                         precision=precision)
+    try:
+        scores, preds = predict_scores(net, splits.val)
+        trained = net.pull_weights()
+    finally:
+        net.release()
+    ref = O.OracleNet(O.OracleNet.from_network(net).layers, [(w, b) for w, b, _, _ in trained])
+    ref_scores, ref_preds = O.predict_scores(ref, splits.val)
+    tol = 1e-5 if precision == "fp32" else 1e-2
+    assert rel(scores, ref_scores) <= tol, f"scores rel {rel(scores, ref_scores):.3e}"
+    margin = 1e-6 if precision == "fp32" else 2e-2
+    clear = np.abs(ref_scores - 0.5) > margin
+    assert np.array_equal(preds[clear], ref_preds[clear])
+    assert preds.dtype == np.int64 and scores.dtype == np.float64
+    assert set(np.unique(preds)) <= {0, 1}
+
+
+def test_predict_ties_go_to_class_0():
+    """All-zero weights give equal logits: argmax must pick class 0 (evaluator.py:185)."""
+    genome = parse_genome("id=tie0000000000000 parents= lr=0.001 momentum=0.9 batch_size=8 f0=pool:size=2,s=2")
+    net = instantiate(genome, (3, 8, 8), seed=0)
+    net.weights = [(np.zeros_like(w), np.zeros_like(b)) for w, b in net.weights]
+    from paper_1909_12291_b200.patches import PatchSet
+    px = np.random.default_rng(0).integers(0, 256, (37, 3, 8, 8)).astype(np.uint8)
+    pset = PatchSet(px, (np.arange(37) % 2).astype(np.uint8))
+    for precision in ("fp32", "bf16"):
+        net.to_device(0, precision, max_batch=128)
+        try:
+            scores, preds = predict_scores(net, pset)
+        finally:
+            net.release()
+        assert not preds.any()
+        np.testing.assert_array_equal(scores, 0.5)
+
+
+def _stack(n_conv):
+    feats = " ".join(f"f{i}=conv:oc=64,k=3,s=1,relu=1" for i in range(n_conv))
+    return parse_genome(f"id=lat{n_conv:013d} parents= lr=0.001 momentum=0.9 batch_size=64 {feats}")
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_latency_deeper_is_slower(precision):
+    """a network with 2x the layers of a fixture has a strictly higher median."""
+    meds = []
+    for n_conv in (3, 6):
+        net = instantiate(_stack(n_conv), (3, 100, 100), seed=0)
+        net.to_device(0, precision, max_batch=64)
+        try:
+            lat = measure_latency(net, 64, reps=5, warmup=1, seed=0)
+        finally:
+            net.release()
+        assert lat.min_s_per_batch <= lat.median_s_per_batch <= lat.max_s_per_batch
+        assert lat.reps == 5 and lat.batch_size == 64
+        assert lat.patches_per_s == pytest.approx(64 / lat.median_s_per_batch)
+        meds.append(lat.median_s_per_batch)
+    assert meds[1] > meds[0], f"6-conv median {meds[1]:.3e} s not above 3-conv {meds[0]:.3e} s"
+
+
+def test_latency_argument_errors():
+    net = instantiate(_stack(1), (3, 20, 20), seed=0)
+    net.to_device(0, "bf16", max_batch=8)
+    try:
+        with pytest.raises(ValueError):
+            measure_latency(net, 8, reps=2)
+        with pytest.raises(ValueError):
+            measure_latency(net, 8, reps=3, warmup=0)
+    finally:
+        net.release()

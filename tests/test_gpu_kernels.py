@@ -79,6 +79,64 @@ def test_conv_passes(shape, precision):
     assert rel(dbd.cpu().numpy(), db_ref) <= tol
 
 
+# (n, c, h, c_out, k, s, pool window, pool stride, relu): packed-like C=8, gather C=16/32, C%64==0,
+# ragged pooled edges, stride > window gaps, more windows than one wave of tiles
+POOL_SHAPES = [(4, 32, 49, 64, 4, 1, 2, 2, 1), (3, 8, 40, 24, 3, 1, 3, 3, 1), (2, 16, 33, 40, 3, 2, 2, 3, 1),
+               (2, 64, 30, 128, 3, 1, 2, 2, 1), (3, 24, 29, 16, 5, 1, 3, 3, 0), (2, 256, 20, 256, 3, 1, 3, 3, 1),
+               (16, 32, 49, 64, 4, 1, 2, 2, 1)]
+
+
+@pytest.mark.parametrize("shape", POOL_SHAPES, ids=[str(s) for s in POOL_SHAPES])
+def test_conv_pool_epilogue(shape):
+    """ce_conv_fwd with the max-pool epilogue == conv then ce_maxpool_fwd, bit for bit (same bf16
+    values compared, same first-max rule), and == the oracle's conv+ReLU+MaxPool (nn.py:82-150)."""
+    n, c, h, co, k, s, pk, ps, relu = shape
+    rng = np.random.default_rng(sum(shape))
+    x = _round(rng.standard_normal((n, c, h, h)), "bf16")
+    w = _round(rng.uniform(-0.2, 0.2, (co, c, k, k)), "bf16")
+    b = rng.uniform(-0.1, 0.1, co).astype(np.float32)
+    oh = (h - k) // s + 1
+    ph = (oh - pk) // ps + 1
+    desc = native.conv_desc(n, c, h, h, co, k, s, "bf16")
+    xd = _dev(x.transpose(0, 2, 3, 1), "bf16")
+    wd = _dev(w.transpose(0, 2, 3, 1), "bf16")
+    bd = torch.from_numpy(b).cuda()
+    yfull = torch.empty((n, oh, oh, co), dtype=torch.bfloat16, device="cuda")
+    yp = torch.full((n, ph, ph, co), 7.0, dtype=torch.bfloat16, device="cuda")
+    argp = torch.full((n, ph, ph, co), 77, dtype=torch.uint8, device="cuda")
+    yu = torch.empty_like(yp)
+    argu = torch.empty_like(argp)
+    st = torch.cuda.current_stream().cuda_stream
+    native.conv_fwd(desc, xd.data_ptr(), wd.data_ptr(), bd.data_ptr(), relu, yp.data_ptr(), st, pool=(pk, ps),
+                    arg=argp.data_ptr())
+    native.conv_fwd(desc, xd.data_ptr(), wd.data_ptr(), bd.data_ptr(), relu, yfull.data_ptr(), st)
+    pdesc = native.conv_desc(n, co, oh, oh, 0, pk, ps, "bf16")
+    native.maxpool_fwd(pdesc, yfull.data_ptr(), yu.data_ptr(), argu.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(yp, yu), "fused pooled values differ from conv + pool"
+    a_f, a_u = argp.cpu().numpy(), argu.cpu().numpy()
+    dead = a_f == 0xFF
+    if relu:
+        assert np.all(yu.float().cpu().numpy()[dead] == 0.0)
+    else:
+        assert not dead.any()
+    np.testing.assert_array_equal(a_f[~dead], a_u[~dead])
+    y_ref = O.conv_forward(x.astype(np.float64), w.astype(np.float64), b.astype(np.float64), s)
+    if relu:
+        y_ref = np.maximum(y_ref, 0)
+    p_ref, _ = O.pool_forward(y_ref, pk, ps)
+    got = yp.float().cpu().numpy().transpose(0, 3, 1, 2)
+    assert rel(got, p_ref) <= 1e-2, f"pooled rel err {rel(got, p_ref):.3e}"
+
+
+def test_conv_pool_epilogue_rejects_overlap():
+    desc = native.conv_desc(1, 8, 10, 10, 8, 3, 1, "bf16")
+    t = torch.zeros(1024, device="cuda")
+    with pytest.raises(Exception):
+        native.conv_fwd(desc, t.data_ptr(), t.data_ptr(), t.data_ptr(), 1, t.data_ptr(), 0, pool=(3, 2),
+                        arg=t.data_ptr())
+
+
 @pytest.mark.parametrize("precision", ["bf16", "fp32"])
 @pytest.mark.parametrize("size,stride", [(2, 1), (2, 2), (2, 3), (3, 1), (3, 2), (3, 3)])
 @pytest.mark.parametrize("variant", ["rand", "ties"])

@@ -50,6 +50,8 @@ def test_forward_backward_step(name, text, shape, precision):
         logits = dev.forward(x)
         ref_logits = oracle.forward(x)
         for li, lshape in enumerate(_layer_shapes(net)):
+            if not dev.materialized(li):  # conv fused with its max-pool: checked through the pool output
+                continue
             got = dev.activation(li, N, lshape)
             err = rel(got, oracle.outs[li])
             assert err <= tol, f"layer {li} activation rel err {err:.3e}"

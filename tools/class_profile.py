@@ -22,7 +22,7 @@ for i, g in enumerate(pop):
     prof = r.extras.get("kernel_profile", {})
     steps = r.extras.get("train_steps", 0)
     parts = []
-    for name, (launches, ms, _, _) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+    for name, (launches, ms, *_) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
         if launches:
             parts.append(f"{name}={ms:.1f}ms/{launches}")
             t = tot.setdefault(name, [0.0, 0])
