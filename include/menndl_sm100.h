@@ -25,6 +25,7 @@
  *   ce_conv_fwd / ce_conv_wgrad / ce_conv_dgrad  <- Conv2d.forward / backward (nn.py:82-116)
  *   ce_maxpool_fwd / ce_maxpool_bwd              <- MaxPool.forward / backward (nn.py:140-167)
  *   ce_dense_fwd / ce_dense_bwd                  <- Dense.forward / backward   (nn.py:225-240)
+ *   ce_relu_fwd / ce_relu_bwd                    <- ReLU.forward / backward    (nn.py:170-183)
  *   ce_softmax_xent                              <- softmax_cross_entropy      (nn.py:287-303)
  *   ce_sgd_momentum                              <- sgd_step, per tensor       (nn.py:306-322)
  *   ce_pcg64_uniform                             <- _kaiming_uniform draws     (nn.py:44-46)
@@ -232,6 +233,12 @@ int ce_softmax_xent(const float* logits, const int64_t* labels, int n, int k, fl
  * (nn.py:308-311) else CE_EINVAL.                                              */
 int ce_sgd_momentum(float* w, float* vel, const float* g, size_t count, float lr, float momentum, void* stream);
 
+/* ReLU (nn.py:170-183) on `count` contiguous elements (bf16 or float32 by precision):
+ * y = x > 0 ? x : 0, mask[i] = (x[i] > 0) as u8 (mask may be NULL); backward
+ * dx = mask ? dy : 0. Pointers 16-byte aligned.                                */
+int ce_relu_fwd(const void* x, size_t count, int precision, void* y, uint8_t* mask, void* stream);
+int ce_relu_bwd(const void* dy, const uint8_t* mask, size_t count, int precision, void* dx, void* stream);
+
 /* numpy Generator(PCG64(state, inc)) advanced by `skip` draws, then
  * .uniform(low, high, size=count).astype(float32) (nn.py:44-46), bit-exact.    */
 int ce_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t skip,
@@ -255,6 +262,9 @@ int ce_net_prof_read(ce_net* net, int cls, const char** name, long long* launche
  * ce_prof_set_peaks (bench.py passes MEASURED_PEAKS.json's sustained bf16 FLOP/s and HBM bytes/s) */
 int ce_prof_set_peaks(double flops_per_s, double bytes_per_s);
 int ce_net_prof_ideal(ce_net* net, int cls, double* ideal_ms);
+/* the same totals for one layer (descriptor index; -1 = batch gather and stand-alone loss) */
+int ce_net_prof_layer(ce_net* net, int layer, int cls, long long* launches, double* ms, double* flops, double* bytes,
+                      double* ideal_ms);
 
 #ifdef __cplusplus
 }

@@ -276,6 +276,7 @@ struct FwdTcEpi {
   // pure-TMA loaders (1 producer warp) leave room for 16 epilogue warps: the bf16
   // store stream is the limit of the wide forwards (gather loaders keep 8: registers)
   static constexpr int EPI_WARPS_TMA = 16;
+  static constexpr int EPI_WARPS_SYNC = 16;  // implicit packed first layer: 8 producer warps, light registers
   bf16* y;
   const float* bias;
   int M, co, relu;
@@ -329,55 +330,82 @@ struct FwdTcEpi {
 };
 
 // Pooled forward epilogue (rows in PoolMap order): bias + ReLU, rounded to the
-// bf16 the unfused path would store, then max + first-max argmax over the KK
-// lanes of each window by warp shuffles (maxpool_fwd_kernel's rule: a later tap
-// wins only if strictly greater; argmax kPoolDead when the window came out of a
-// ReLU and its max is not > 0). The window's tap-0 lane stores the pooled bf16
-// value and the u8 argmax in NHWC order of the pooled map.
+// bf16 the unfused path would store; each warp stages its 32 rows x 16 columns
+// in shared memory and then every lane reduces (window, column) pairs over the
+// window's KK rows: max with maxpool_fwd_kernel's first-max rule (a later tap
+// wins only if strictly greater), argmax kPoolDead when the window came out of
+// a ReLU and its max is not > 0. Stores the pooled bf16 value and the u8
+// argmax in NHWC order of the pooled map (half-warps write 32 contiguous bytes).
 template <int KK>
 struct FwdPoolEpi {
+  // the epilogue reads KK rows per output: 16 warps (4 per scheduler) keep it from limiting the kernel
+  static constexpr int EPI_WARPS = 16;
   static constexpr int WPW = 32 / KK;
+  static constexpr int ROW = 24;                 // staged row stride in bf16 (48 B: conflict-free window reads)
+  static constexpr int WARP_SMEM = 32 * ROW * 2;  // per epilogue warp
   bf16* y;       // pooled [windows][co]
   uint8_t* arg;  // [windows][co]
   const float* bias;
   int co, relu;
   PoolMap pm;
-  __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
-    const int lane = row & 31;
-    const int wl = lane / KK, tap = lane - wl * KK, base = wl * KK;
-    const int window = (c.m0 / TC_BM) * (4 * WPW) + (row >> 5) * WPW + wl;
+  __device__ void store_warp(const TileCoord& c, int q, int col, const float (&v)[16], uint8_t* scratch) const {
+    const int lane = threadIdx.x & 31;
     const int o0 = c.n0 + col;
-    float best[16];
-    uint8_t bi[16];
+    bf16* st = (bf16*)scratch;
+    {
+      float bv[16];
+      if (o0 + 16 <= co) {  // co % 8 == 0, o0 % 16 == 0: 16-byte aligned
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float t = v[i] + (o0 + i < co ? __ldg(bias + o0 + i) : 0.f);
-      if (relu) t = t > 0.f ? t : 0.f;
-      t = __bfloat162float(__float2bfloat16_rn(t));
-      float bv = __shfl_sync(0xffffffffu, t, base);
+        for (int h = 0; h < 4; ++h) {
+          const float4 b4 = __ldg((const float4*)(bias + o0) + h);
+          bv[4 * h] = b4.x; bv[4 * h + 1] = b4.y; bv[4 * h + 2] = b4.z; bv[4 * h + 3] = b4.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) bv[i] = o0 + i < co ? __ldg(bias + o0 + i) : 0.f;
+      }
+      uint32_t r[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float t0 = v[2 * i] + bv[2 * i], t1 = v[2 * i + 1] + bv[2 * i + 1];
+        if (relu) {
+          t0 = t0 > 0.f ? t0 : 0.f;
+          t1 = t1 > 0.f ? t1 : 0.f;
+        }
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(t0, t1);
+        r[i] = *(const uint32_t*)&h2;
+      }
+      uint4* dst = (uint4*)(st + lane * ROW);
+      dst[0] = make_uint4(r[0], r[1], r[2], r[3]);
+      dst[1] = make_uint4(r[4], r[5], r[6], r[7]);
+    }
+    __syncwarp();
+    const int window0 = (c.m0 / TC_BM) * (4 * WPW) + q * WPW;
+#pragma unroll
+    for (int p = lane; p < WPW * 16; p += 32) {
+      const int wl = p >> 4, cc = p & 15;
+      const int window = window0 + wl, o = o0 + cc;
+      const bf16* src = st + wl * KK * ROW + cc;
+      bf16 bb = src[0];
+      float bv = __bfloat162float(bb);
       int b = 0;
 #pragma unroll
       for (int k = 1; k < KK; ++k) {
-        const float u = __shfl_sync(0xffffffffu, t, base + k);
+        const bf16 ub = src[k * ROW];
+        const float u = __bfloat162float(ub);
         if (u > bv) {
           bv = u;
+          bb = ub;
           b = k;
         }
       }
-      best[i] = bv;
-      bi[i] = (relu && !(bv > 0.f)) ? kPoolDead : (uint8_t)b;
+      if (window < pm.windows && o < co) {
+        const size_t off = (size_t)window * co + o;
+        y[off] = bb;
+        arg[off] = (relu && !(bv > 0.f)) ? kPoolDead : (uint8_t)b;
+      }
     }
-    if (tap != 0 || wl >= WPW || window >= pm.windows || o0 >= co) return;
-    const size_t off = (size_t)window * co + o0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (o0 + 8 * h >= co) break;
-      __align__(16) bf16 out[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = __float2bfloat16_rn(best[8 * h + i]);
-      *(uint4*)(y + off + 8 * h) = *(const uint4*)out;
-      *(uint2*)(arg + off + 8 * h) = *(const uint2*)&bi[8 * h];
-    }
+    __syncwarp();
   }
   __device__ void finish(int, int) const {}
 };

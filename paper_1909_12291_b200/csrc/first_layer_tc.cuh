@@ -173,6 +173,203 @@ inline void launch_pool_expand_rows(const T* dyp, const uint8_t* arg, const Pool
   pool_expand_rows_kernel<T><<<grid_for((size_t)rows * (co / 8)), 256, 0, st>>>(dyp, arg, pm, co, rows, dy);
 }
 
+inline int conv_wgrad_packed_splits(int Kp, int Mo, int num_sms) {
+  const int m_tiles = (Kp + TC_BM - 1) / TC_BM;
+  const long long nkb = ((long long)Mo + TC_BK - 1) / TC_BK;
+  long long want = num_sms / m_tiles;
+  if (want > nkb / 4) want = nkb / 4;
+  if (want > 128) want = 128;
+  return want < 1 ? 1 : (int)want;
+}
+
+// ------------------------------------------------------------------ implicit packed operand
+// The packed im2col row of an output pixel, xrow[kk] (kk = (i*k + j)*c_real + c
+// < Kr, xrow[Kr] = 1, zero to Kp), is built by the producer warps straight from
+// the channel-padded input into the stage's shared-memory tile: no im2col
+// matrix in HBM (it would cost Kp*2 bytes per pixel twice, k^2-fold the input).
+//   fwd   (MN = false): A = xrow, K-major [128 pixels][64 kk] per k-block; B = Wp
+//         by 2D TMA. Epilogue as conv_fwd_packed (bias/ReLU, or the pooled one).
+//   wgrad (MN = true) : A = xrow^T, MN-major [128 kk][64 pixels]; B = dY [pixels][co]
+//         by 64x64 TMA boxes (BN >= 64) or plain loads. Row Kr of D = sum dY = db.
+// POOL: pixels in the window-major PoolMap order (padding rows all zero, the ones
+// column included, so they add nothing to D).
+template <bool MN, bool POOL, bool TMA_B>
+struct PackedTcLoader {
+  static constexpr int A_MN_MAJOR = MN, B_MN_MAJOR = MN;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B, PURE_TMA = false, SYNC_FILL = true;
+  CUtensorMap bmap;  // fwd: Wp [co][Kp]; wgrad: dY [rows][co] (TMA_B)
+  const bf16* x;     // channel-padded input [n][h][w][8]
+  const bf16* dy;    // wgrad without TMA_B
+  ConvGeom g;
+  int c_real, Kr, Kp, rows, BN;
+  FastDiv d_ow, d_oh;
+  PoolMap pm;
+  __device__ void init(uint8_t* table, int tid, int nthreads) const {
+    int* off = (int*)table;
+    for (int kk = tid; kk < Kp; kk += nthreads) {
+      if (kk < Kr) {
+        const int tap = kk / c_real, c = kk - tap * c_real;
+        const int i = tap / g.k, j = tap - i * g.k;
+        off[kk] = (i * g.w + j) * g.c + c;
+      } else {
+        off[kk] = kk == Kr ? -1 : -2;
+      }
+    }
+  }
+  // input offset of the receptive-field origin of GEMM row m, or -1 for a padding row
+  __device__ __forceinline__ long long origin(int m) const {
+    uint32_t n, p, q, t;
+    if constexpr (POOL) {
+      if (!pm.pixel(m / TC_BM, m % TC_BM, n, p, q)) return -1;
+    } else {
+      if (m >= rows) return -1;
+      d_ow.divmod((uint32_t)m, t, q);
+      d_oh.divmod(t, n, p);
+    }
+    return (((long long)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
+  }
+  // 8 consecutive xrow values from kk0 (kk0 % 8 == 0) of the row at `base`, packed bf16x2
+  __device__ __forceinline__ uint4 chunk(long long base, int kk0, const int* off) const {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    if (base >= 0 && kk0 < Kp) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int o = off[kk0 + u];
+        v[u] = o >= 0 ? __bfloat162float(x[base + o]) : (o == -1 ? 1.f : 0.f);
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
+        w[h] = *(const uint32_t*)&b2;
+      }
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
+                       uint64_t* full) const {
+    const int* off = (const int*)table;
+    if constexpr (!MN) {
+      if (ptid == 0) {
+        mbar_expect_tx(full, (uint32_t)BN * 128u);
+        tma_load_2d(sB, &bmap, kb * TC_BK, c.n0, full);
+      }
+      // only the K16 steps the MMA issues are filled (Kp < 64: a single K block)
+      const int kcs = min(8, ((Kp - kb * TC_BK + 15) / 16) * 2);
+      const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;
+      const long long base = origin(c.m0 + r);
+      uint4 vals[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kc = kc0 + 2 * e;
+        vals[e] = kc < kcs ? chunk(base, kb * TC_BK + kc * 8, off) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kc = kc0 + 2 * e;
+        if (kc < kcs) st_shared_v4(sA + kmajor_off(TC_BM, r, kc), vals[e]);
+      }
+    } else {
+      // A: 16 groups of 8 kk rows x 64 pixels; 256 producers -> 4 (group, pixel) chunks each
+      const int grp = ptid & 15;
+      const int kk0 = c.m0 + grp * 8;
+      uint4 vals[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kr = (ptid >> 4) + e * 16;
+        vals[e] = chunk(origin(kb * TC_BK + kr), kk0, off);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) st_shared_v4(sA + mnmajor_off(TC_BM, grp, (ptid >> 4) + e * 16), vals[e]);
+      if constexpr (TMA_B) {
+        if (ptid == 0) {
+          mbar_expect_tx(full, (uint32_t)BN * TC_BK * 2u);
+          for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &bmap, c.n0 + 64 * j, kb * TC_BK, full);
+        }
+      } else {
+        const int groups = BN / 8;
+        for (int ch = ptid; ch < groups * TC_BK; ch += TC_PRODUCERS) {
+          const int gq = ch % groups, kr = ch / groups;
+          const int o0 = c.n0 + gq * 8, m = kb * TC_BK + kr;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (o0 < g.co && m < rows) v = *(const uint4*)(dy + (size_t)m * g.co + o0);
+          st_shared_v4(sB + mnmajor_off(BN, gq, kr), v);
+        }
+      }
+    }
+  }
+};
+
+// Packed first-layer forward without the HBM im2col (PackedTcLoader); pm: pooled epilogue
+inline int conv_fwd_packed_implicit(const ConvGeom& g, const bf16* x, int c_real, int Kp, const bf16* wp,
+                                    const float* bias, int relu, const PoolMap* pm, bf16* y, uint8_t* arg,
+                                    int num_sms, cudaStream_t st) {
+  const int M = pm ? pool_rows(*pm) : g.n * g.oh * g.ow;
+  return with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.co, num_sms), [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(M, g.co, Kp, BN, 1);
+    auto fill = [&](auto& ld) {
+      ld.x = x; ld.g = g; ld.c_real = c_real; ld.Kr = packed_kr(g, c_real); ld.Kp = Kp; ld.rows = M; ld.BN = BN;
+      ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      if (pm) ld.pm = *pm;
+      return make_tmap_kmajor(&ld.bmap, wp, g.co, Kp, BN);
+    };
+    cudaError_t e;
+    if (pm) {
+      PackedTcLoader<false, true, true> ld{};
+      if (!fill(ld)) return fail(CE_ECUDA, "conv_fwd_packed_implicit: tensor map encoding failed");
+      e = (cudaError_t)with_pool_kk(pm->ps, [&](auto kkc) {
+        constexpr int KK = decltype(kkc)::value;
+        return (int)tc_launch<BN>(ld, FwdPoolEpi<KK>{y, arg, bias, g.co, relu, *pm}, sh, num_sms, st);
+      });
+    } else {
+      PackedTcLoader<false, false, true> ld{};
+      if (!fill(ld)) return fail(CE_ECUDA, "conv_fwd_packed_implicit: tensor map encoding failed");
+      e = tc_launch<BN>(ld, FwdTcEpi{y, bias, M, g.co, relu}, sh, num_sms, st);
+    }
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_packed_implicit: %s", cudaGetErrorString(e));
+  });
+}
+
+// Packed first-layer weight gradient without the HBM im2col: part[split][co][Kp]
+inline int conv_wgrad_packed_implicit(const ConvGeom& g, const bf16* x, int c_real, int Kp, const bf16* dy,
+                                      const PoolMap* pm, float* part, int* splits_out, int num_sms, cudaStream_t st) {
+  const int Mo = pm ? pool_rows(*pm) : g.n * g.oh * g.ow;
+  return with_bn(g.co, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(Kp, g.co, Mo, BN, conv_wgrad_packed_splits(Kp, Mo, num_sms));
+    *splits_out = sh.splits;
+    WgradTcEpi ep{part, Kp, g.co};
+    auto run = [&](auto& ld) {
+      ld.x = x; ld.dy = dy; ld.g = g; ld.c_real = c_real; ld.Kr = packed_kr(g, c_real); ld.Kp = Kp; ld.rows = Mo;
+      ld.BN = BN; ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      if (pm) ld.pm = *pm;
+      return tc_launch<BN>(ld, ep, sh, num_sms, st);
+    };
+    cudaError_t e;
+    if constexpr (BN >= 64) {
+      if (pm) {
+        PackedTcLoader<true, true, true> ld{};
+        if (!make_tmap_mn64(&ld.bmap, dy, Mo, g.co)) return fail(CE_ECUDA, "conv_wgrad_packed_implicit: tmap");
+        e = run(ld);
+      } else {
+        PackedTcLoader<true, false, true> ld{};
+        if (!make_tmap_mn64(&ld.bmap, dy, Mo, g.co)) return fail(CE_ECUDA, "conv_wgrad_packed_implicit: tmap");
+        e = run(ld);
+      }
+    } else {
+      if (pm) {
+        PackedTcLoader<true, true, false> ld{};
+        e = run(ld);
+      } else {
+        PackedTcLoader<true, false, false> ld{};
+        e = run(ld);
+      }
+    }
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_wgrad_packed_implicit: %s", cudaGetErrorString(e));
+  });
+}
+
 // A = xcol^T (MN-major over kk, 64x64 TMA boxes); B = dY (MN-major over C_out):
 // TMA boxes when C_out >= 64, else cp.async chunks gathered by the producers.
 template <bool TMA_B>
@@ -205,14 +402,6 @@ struct WgradPackedLoader {
   }
 };
 
-inline int conv_wgrad_packed_splits(int Kp, int Mo, int num_sms) {
-  const int m_tiles = (Kp + TC_BM - 1) / TC_BM;
-  const long long nkb = ((long long)Mo + TC_BK - 1) / TC_BK;
-  long long want = num_sms / m_tiles;
-  if (want > nkb / 4) want = nkb / 4;
-  if (want > 128) want = 128;
-  return want < 1 ? 1 : (int)want;
-}
 
 // part[split][co][Kp]: split-K partial sums of D^T (row Kr = bias gradient)
 // rows: reduction length (default n*oh*ow; pool_rows() for the window-major order)

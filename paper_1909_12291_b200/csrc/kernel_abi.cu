@@ -328,6 +328,85 @@ int ce_sgd_momentum(float* w, float* vel, const float* g, size_t count, float lr
   return CE_OK;
 }
 
+}  // extern "C"
+
+// ReLU of the operator API (nn.py:170-183): y = x > 0 ? x : 0 and the u8 mask (x > 0);
+// backward dx = dy * mask. T = bf16 or float; 8 elements per thread when aligned.
+template <class T>
+__global__ void __launch_bounds__(256) relu_fwd_kernel(const T* __restrict__ x, size_t count, T* __restrict__ y,
+                                                       uint8_t* __restrict__ mask) {
+  const size_t n8 = count / 8;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n8; e += (size_t)gridDim.x * blockDim.x) {
+    float v[8];
+    load8(x + e * 8, v);
+    uint8_t m[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      m[u] = v[u] > 0.f;
+      v[u] = m[u] ? v[u] : 0.f;
+    }
+    store8(y + e * 8, v);
+    if (mask) *(uint2*)(mask + e * 8) = *(const uint2*)m;
+  }
+  for (size_t e = n8 * 8 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const float v = ldf(x, e);
+    const bool pos = v > 0.f;
+    stf(y, e, pos ? v : 0.f);
+    if (mask) mask[e] = pos;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) relu_bwd_kernel(const T* __restrict__ dy, const uint8_t* __restrict__ mask,
+                                                       size_t count, T* __restrict__ dx) {
+  const size_t n8 = count / 8;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n8; e += (size_t)gridDim.x * blockDim.x) {
+    float v[8];
+    load8(dy + e * 8, v);
+    const uint2 m2 = *(const uint2*)(mask + e * 8);
+    const uint8_t* m = (const uint8_t*)&m2;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = m[u] ? v[u] : 0.f;
+    store8(dx + e * 8, v);
+  }
+  for (size_t e = n8 * 8 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count;
+       e += (size_t)gridDim.x * blockDim.x)
+    stf(dx, e, mask[e] ? ldf(dy, e) : 0.f);
+}
+
+extern "C" {
+
+int ce_relu_fwd(const void* x, size_t count, int precision, void* y, uint8_t* mask, void* stream) {
+  if (count == 0) return CE_OK;
+  if (!x || !y) return fail(CE_EINVAL, "null relu operand");
+  if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)mask) & 15) return fail(CE_EINVAL, "relu operands must be 16-byte aligned");
+  const size_t g = grid_for((count + 7) / 8);
+  if (precision == CE_PREC_BF16)
+    relu_fwd_kernel<bf16><<<g, 256, 0, (cudaStream_t)stream>>>((const bf16*)x, count, (bf16*)y, mask);
+  else if (precision == CE_PREC_FP32)
+    relu_fwd_kernel<float><<<g, 256, 0, (cudaStream_t)stream>>>((const float*)x, count, (float*)y, mask);
+  else
+    return fail(CE_EINVAL, "bad precision %d", precision);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
+int ce_relu_bwd(const void* dy, const uint8_t* mask, size_t count, int precision, void* dx, void* stream) {
+  if (count == 0) return CE_OK;
+  if (!dy || !mask || !dx) return fail(CE_EINVAL, "null relu operand");
+  if (((uintptr_t)dy | (uintptr_t)dx | (uintptr_t)mask) & 15) return fail(CE_EINVAL, "relu operands must be 16-byte aligned");
+  const size_t g = grid_for((count + 7) / 8);
+  if (precision == CE_PREC_BF16)
+    relu_bwd_kernel<bf16><<<g, 256, 0, (cudaStream_t)stream>>>((const bf16*)dy, mask, count, (bf16*)dx);
+  else if (precision == CE_PREC_FP32)
+    relu_bwd_kernel<float><<<g, 256, 0, (cudaStream_t)stream>>>((const float*)dy, mask, count, (float*)dx);
+  else
+    return fail(CE_EINVAL, "bad precision %d", precision);
+  CE_CHECK_LAUNCH();
+  return CE_OK;
+}
+
 int ce_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t skip,
                      double low, double high, float* out, size_t count, void* stream) {
   if (count == 0) return CE_OK;

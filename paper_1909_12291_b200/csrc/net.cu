@@ -14,6 +14,7 @@
 #include <cmath>
 #include <atomic>
 #include <condition_variable>
+#include <map>
 #include <mutex>
 #include "ops.cuh"
 #include "conv_tc.cuh"
@@ -93,7 +94,7 @@ enum ProfClass { P_CONV_FWD = 0, P_CONV_DGRAD, P_CONV_WGRAD, P_CONV_SGD, P_DENSE
 static const char* kProfNames[P_NCLASS] = {"conv_fwd", "conv_dgrad", "conv_wgrad", "conv_sgd", "dense_fwd",
                                            "dense_bwd", "pool", "loss", "gather"};
 struct ProfEvent {
-  int cls;
+  int cls, layer;
   double flops, bytes;
   cudaEvent_t a, b;
 };
@@ -111,6 +112,8 @@ struct ce_net {
   bool prof_on = false;
   std::vector<ProfEvent> prof_pending;
   ProfTotals prof[P_NCLASS];
+  std::map<std::pair<int, int>, ProfTotals> prof_layers;  // (layer, class) -> totals; layer -1 = gather / loss
+  int prof_layer_cur = -1;                                 // layer being enqueued (set by the layer loops)
   long long acc = 0;  // kernels enqueued since the last reset
   cudaStream_t st = nullptr;
   int in_c = 3, in_cp = 8, in_h = 100, in_w = 100, max_batch = 0, classes = 2;
@@ -292,9 +295,10 @@ struct Prof {
   ce_net* net;
   int cls;
   double flops, bytes;
-  int kernels;
+  int kernels, layer;
   cudaEvent_t a = nullptr;
-  Prof(ce_net* n, int c, double f, double b, int k = 1) : net(n), cls(c), flops(f), bytes(b), kernels(k) {
+  Prof(ce_net* n, int c, double f, double b, int k = 1)
+      : net(n), cls(c), flops(f), bytes(b), kernels(k), layer(n->prof_layer_cur) {
     net->acc += k;
     if (net->prof_on) {
       cudaEventCreate(&a);
@@ -306,7 +310,7 @@ struct Prof {
       cudaEvent_t b;
       cudaEventCreate(&b);
       cudaEventRecord(b, net->st);
-      net->prof_pending.push_back(ProfEvent{cls, flops, bytes, a, b});
+      net->prof_pending.push_back(ProfEvent{cls, layer, flops, bytes, a, b});
     }
   }
 };
@@ -316,12 +320,14 @@ void prof_collect(ce_net* net) {
     float ms = 0.f;
     cudaEventSynchronize(e.b);
     cudaEventElapsedTime(&ms, e.a, e.b);
-    ProfTotals& t = net->prof[e.cls];
-    t.launches += 1;
-    t.ms += ms;
-    t.flops += e.flops;
-    t.bytes += e.bytes;
-    t.ideal_ms += 1e3 * std::max(e.flops / g_peak_flops, e.bytes / g_peak_bytes);
+    const double ideal = 1e3 * std::max(e.flops / g_peak_flops, e.bytes / g_peak_bytes);
+    for (ProfTotals* t : {&net->prof[e.cls], &net->prof_layers[{e.layer, e.cls}]}) {
+      t->launches += 1;
+      t->ms += ms;
+      t->flops += e.flops;
+      t->bytes += e.bytes;
+      t->ideal_ms += ideal;
+    }
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
@@ -367,6 +373,7 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
   bool in_act = true;
   for (size_t li = 0; li < net->L.size(); ++li) {
     Layer& l = net->L[li];
+    net->prof_layer_cur = (int)li;
     if (l.kind == CE_LAYER_CONV && l.pool_fused) {  // conv + max-pool in one GEMM epilogue
       ConvGeom g = l.g;
       g.n = n;
@@ -376,11 +383,9 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
       const double ab = (double)act_bytes(net), pooled = (double)pm.windows * g.co;
       Prof pf(net, P_CONV_FWD, 2.0 * pm.windows * pm.KK * g.co * g.k * g.k * l.c_real,
               ab * ((double)n * g.h * g.w * g.c + pooled + (double)g.co * K) + pooled + 4.0 * g.co, l.packed ? 2 : 1);
-      if (l.packed) {
-        launch_im2col_packed((const T*)in, g, l.c_real, l.Kp, (T*)l.xcol, st, &pm);
-        CE_CHECK_LAUNCH();
-        int s = conv_fwd_packed_pool(g, (const bf16*)l.xcol, l.Kp, l.Wp, l.b, l.relu, pm, (bf16*)pl.out, pl.arg,
-                                     net->num_sms, st);
+      if (l.packed) {  // implicit packed operand: no im2col matrix in HBM
+        int s = conv_fwd_packed_implicit(g, (const bf16*)in, l.c_real, l.Kp, l.Wp, l.b, l.relu, &pm, (bf16*)pl.out,
+                                         pl.arg, net->num_sms, st);
         if (s != CE_OK) return s;
       } else {
         int s = conv_fwd_tc_pool(g, (const bf16*)in, l.Wbf, l.b, l.relu, pl.g.k, pl.g.s, (bf16*)pl.out, pl.arg,
@@ -401,12 +406,13 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
       Prof pf(net, P_CONV_FWD, 2.0 * M * g.co * g.k * g.k * l.c_real,
               ab * ((double)n * g.h * g.w * g.c + (double)M * g.co + (double)g.co * K) + 4.0 * g.co);
       if (l.packed) {
-        launch_im2col_packed((const T*)in, g, l.c_real, l.Kp, (T*)l.xcol, st);
-        CE_CHECK_LAUNCH();
-        if (net->use_tc) {
-          int s = conv_fwd_packed(g, (const bf16*)l.xcol, l.Kp, l.Wp, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
+        if (net->use_tc) {  // implicit packed operand: no im2col matrix in HBM
+          int s = conv_fwd_packed_implicit(g, (const bf16*)in, l.c_real, l.Kp, l.Wp, l.b, l.relu, nullptr,
+                                           (bf16*)l.out, nullptr, net->num_sms, st);
           if (s != CE_OK) return s;
-        } else {
+        } else {  // fp32 check mode: explicit im2col + CUDA-core GEMM
+          launch_im2col_packed((const T*)in, g, l.c_real, l.Kp, (T*)l.xcol, st);
+          CE_CHECK_LAUNCH();
           conv_fwd_packed_simt(g, (const float*)l.xcol, l.Kp, l.Wpf, l.b, l.relu, (float*)l.out, st);
         }
       } else if (net->use_tc) {
@@ -499,6 +505,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
   const bool keep = net->keep_grads;
   for (int li = (int)net->L.size() - 1; li >= 0; --li) {
     Layer& l = net->L[li];
+    net->prof_layer_cur = li;
     const void* x = li == 0 ? net->x0 : net->L[li - 1].out;
     const void* gin = net->gbuf[cur];
     void* gout = net->gbuf[cur ^ 1];
@@ -616,11 +623,12 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
         while (splits > 1 && (size_t)splits * g.co * l.Kp * 4 > net->ws_bytes) splits = simt_splits((int)Mo_, splits - 1);
         conv_wgrad_packed_simt(g, (const float*)l.xcol, l.Kp, (const float*)dy, net->ws, splits, st);
       } else if (l.packed) {
-        const int rows = l.pool_fused ? pool_rows(layer_pool_map(net, li, n)) : Mo;
-        int s = conv_wgrad_packed(g, (const bf16*)l.xcol, l.Kp, (const bf16*)dy, net->ws, &splits, net->num_sms, st,
-                                  rows);
+        const PoolMap pm = l.pool_fused ? layer_pool_map(net, li, n) : PoolMap{};
+        const int rows = l.pool_fused ? pool_rows(pm) : Mo;
+        int s = conv_wgrad_packed_implicit(g, (const bf16*)x, l.c_real, l.Kp, (const bf16*)dy,
+                                           l.pool_fused ? &pm : nullptr, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
-        pf.bytes = ab * ((double)rows * g.co + (double)rows * l.Kp) + 4.0 * splits * g.co * l.Kp;
+        pf.bytes = ab * ((double)rows * g.co + (double)n * g.h * g.w * g.c) + 4.0 * splits * g.co * l.Kp;
       } else if (net->use_tc) {
         int s = conv_wgrad_tc(g, (const bf16*)x, (const bf16*)dy, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
@@ -685,6 +693,7 @@ int enqueue_step(ce_net* net, int n, float lr, float mu) {
   int s = enqueue_forward<T>(net, n, true, &loss_fused);
   if (s != CE_OK) return s;
   const Layer& last = net->L.back();
+  net->prof_layer_cur = -1;
   if (!loss_fused) {
     Prof pf(net, P_LOSS, 0.0, 16.0 * n * net->classes);
     xent_kernel<int32_t><<<1, 1024, 0, net->st>>>((const float*)last.out, net->ybatch, n, net->classes,
@@ -705,6 +714,7 @@ int gather_any(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_per
                bool labels) {
   dim3 grid = gather_grid(ds->h * ds->w, B);
   int HW = ds->h * ds->w;
+  net->prof_layer_cur = -1;
   Prof pf(net, P_GATHER, 0.0, (double)B * HW * (ds->c + net->in_cp * act_bytes(net)));
   if (net->prec == CE_PREC_FP32)
     gather_u8_kernel<float><<<grid, 256, 0, net->st>>>(ds->pix, ds->lab, perm, net->d_step, n_perm, spe, base, B,
@@ -773,8 +783,23 @@ int ce_prof_num_classes(void) { return P_NCLASS; }
 int ce_net_set_profiling(ce_net* net, int on) {
   if (!net) return fail(CE_EINVAL, "null net");
   net->prof_on = on != 0;
-  if (on)
+  if (on) {
     for (auto& t : net->prof) t = ProfTotals();
+    net->prof_layers.clear();
+  }
+  return CE_OK;
+}
+
+int ce_net_prof_layer(ce_net* net, int layer, int cls, long long* launches, double* ms, double* flops, double* bytes,
+                      double* ideal_ms) {
+  if (!net || cls < 0 || cls >= P_NCLASS) return fail(CE_EINVAL, "bad profile class %d", cls);
+  auto it = net->prof_layers.find({layer, cls});
+  const ProfTotals t = it == net->prof_layers.end() ? ProfTotals() : it->second;
+  if (launches) *launches = t.launches;
+  if (ms) *ms = t.ms;
+  if (flops) *flops = t.flops;
+  if (bytes) *bytes = t.bytes;
+  if (ideal_ms) *ideal_ms = t.ideal_ms;
   return CE_OK;
 }
 
@@ -1023,7 +1048,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
           const int psp = conv_wgrad_packed_splits(l.Kp, (int)rows, net->num_sms);
           ws = std::max(ws, (size_t)psp * l.g.co * l.Kp * 4);
           max_g = std::max(max_g, (size_t)rows * l.g.co * ab);  // window-major dY of the fused pool
-          ALLOC(l.xcol, (size_t)rows * l.Kp * ab);
+          if (precision == CE_PREC_FP32) ALLOC(l.xcol, (size_t)rows * l.Kp * ab);  // bf16: implicit operand
           if (precision == CE_PREC_FP32) {
             ALLOC(l.Wpf, (size_t)l.g.co * l.Kp * 4);
             ws = std::max(ws, (size_t)simt_splits((int)Mo, pick_splits(simt_tiles(l.g.co, l.Kp), Mo, 512,

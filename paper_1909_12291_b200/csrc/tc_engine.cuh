@@ -64,14 +64,48 @@ struct EpiWarpsTma<Epi, std::void_t<decltype(Epi::EPI_WARPS_TMA)>> {
   static constexpr int value = Epi::EPI_WARPS_TMA;
 };
 
+// Epi::WARP_SMEM: bytes of shared-memory scratch per epilogue warp for epilogues
+// that combine rows (the pooled forward); the engine then calls
+// epi.store_warp(c, quarter, col, v, scratch) instead of epi.store.
+template <class Epi, class = void>
+struct EpiWarpSmem {
+  static constexpr int value = 0;
+};
+template <class Epi>
+struct EpiWarpSmem<Epi, std::void_t<decltype(Epi::WARP_SMEM)>> {
+  static constexpr int value = Epi::WARP_SMEM;
+};
+
+// Loader::SYNC_FILL: the producers write the stage with plain shared-memory
+// stores (values computed in registers, e.g. the implicit packed im2col of the
+// first layer); the engine fences them to the async proxy and arrives right
+// after load() instead of tracking cp.async groups.
+template <class Loader, class = void>
+struct SyncFill : std::false_type {};
+template <class Loader>
+struct SyncFill<Loader, std::void_t<decltype(Loader::SYNC_FILL)>> : std::bool_constant<Loader::SYNC_FILL> {};
+
+// Epi::EPI_WARPS_SYNC: epilogue warps when the loader fills stages with st.shared (SyncFill)
+template <class Epi, class = void>
+struct EpiWarpsSync {
+  static constexpr int value = 0;
+};
+template <class Epi>
+struct EpiWarpsSync<Epi, std::void_t<decltype(Epi::EPI_WARPS_SYNC)>> {
+  static constexpr int value = Epi::EPI_WARPS_SYNC;
+};
+
 template <class Loader, class Epi>
 struct TcRoles {
   static constexpr int PW = ProducerWarps<Loader>::value;
-  static constexpr int EW =
-      (Loader::PURE_TMA && EpiWarpsTma<Epi>::value) ? EpiWarpsTma<Epi>::value : EpiWarps<Epi>::value;
+  static constexpr int EW = (Loader::PURE_TMA && EpiWarpsTma<Epi>::value)        ? EpiWarpsTma<Epi>::value
+                            : (SyncFill<Loader>::value && EpiWarpsSync<Epi>::value) ? EpiWarpsSync<Epi>::value
+                                                                                   : EpiWarps<Epi>::value;
   static constexpr int MMA_WARP = PW + EW;
   static constexpr int THREADS = (MMA_WARP + 1) * 32;
   static_assert(EW % 4 == 0, "epilogue warps must cover the 4 TMEM lane quarters equally");
+  // shared-memory staging of the epilogue warps (STAGED_BF16: 1 KB each; WARP_SMEM scratch)
+  static constexpr int EPI_STAGE = EpiStaged<Epi>::value ? EW * 1024 : EW * EpiWarpSmem<Epi>::value;
 };
 constexpr int TC_TABLE_BYTES = 20480;              // loader lookup tables
 constexpr int TC_MAX_LAG = 8;
@@ -144,7 +178,8 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Loader ld, const __grid_constant__ Epi epi, const TcShape shape) {
   using R = TcRoles<Loader, Epi>;
   constexpr bool STAGED = EpiStaged<Epi>::value;
-  using L = TcSmemLayout<BN, STAGED ? R::EW * 1024 : 0>;
+  constexpr int WSM = EpiWarpSmem<Epi>::value;
+  using L = TcSmemLayout<BN, R::EPI_STAGE>;
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -154,7 +189,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base_slot = (uint32_t*)(tempty + 2);
-  uint8_t* epi_stage = table + TC_TABLE_BYTES + L::BAR_BYTES;  // STAGED: 1 KB per epilogue warp (16-B aligned)
+  uint8_t* epi_stage = table + TC_TABLE_BYTES + L::BAR_BYTES;  // epilogue warp staging / scratch (16-B aligned)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -196,6 +231,10 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
         const uint32_t sB = sA + L::A_BYTES;
         if (Loader::PURE_TMA) {  // copies complete on the barrier themselves
           ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
+          mbar_arrive(&full[stage]);
+        } else if constexpr (SyncFill<Loader>::value) {  // st.shared fill: visible to the MMA after the fence
+          ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
+          fence_proxy_async();
           mbar_arrive(&full[stage]);
         } else {
           ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
@@ -283,7 +322,10 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
           float v[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-          epi.store(c, row_in_tile, col, v);
+          if constexpr (WSM > 0)
+            epi.store_warp(c, q, col, v, epi_stage + (warp - R::PW) * WSM);
+          else
+            epi.store(c, row_in_tile, col, v);
         }
       }
       tc_fence_before();
@@ -360,7 +402,7 @@ __device__ __forceinline__ uint32_t mnmajor_off(int R, int g, int kk) {
 
 template <int BN, class Loader, class Epi>
 inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& shape, int num_sms, cudaStream_t st) {
-  using L = TcSmemLayout<BN, EpiStaged<Epi>::value ? TcRoles<Loader, Epi>::EW * 1024 : 0>;
+  using L = TcSmemLayout<BN, TcRoles<Loader, Epi>::EPI_STAGE>;
   auto kern = tc_gemm_kernel<BN, Loader, Epi>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
   if (e != cudaSuccess) return e;

@@ -86,6 +86,8 @@ _SIGNATURES = {
                       C.c_size_t, _P], C.c_int),
     "ce_softmax_xent": ([_P, _P, C.c_int, C.c_int, _P, _P, _P], C.c_int),
     "ce_sgd_momentum": ([_P, _P, _P, C.c_size_t, C.c_float, C.c_float, _P], C.c_int),
+    "ce_relu_fwd": ([_P, C.c_size_t, C.c_int, _P, _P, _P], C.c_int),
+    "ce_relu_bwd": ([_P, _P, C.c_size_t, C.c_int, _P, _P], C.c_int),
     "ce_pcg64_uniform": ([C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_double, _P,
                           C.c_size_t, _P], C.c_int),
     "ce_permute_flatten_weights": ([_P, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
@@ -95,6 +97,7 @@ _SIGNATURES = {
     "ce_net_prof_read": ([_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_longlong), _D, _D, _D], C.c_int),
     "ce_prof_set_peaks": ([C.c_double, C.c_double], C.c_int),
     "ce_net_prof_ideal": ([_P, C.c_int, _D], C.c_int),
+    "ce_net_prof_layer": ([_P, C.c_int, C.c_int, C.POINTER(C.c_longlong), _D, _D, _D, _D], C.c_int),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -191,6 +194,14 @@ def dense_bwd(desc, x, dy, w, w16, b, dx, mask, dw, db, sgd, ws, ws_bytes, strea
 
 def softmax_xent(logits, labels, n, k, loss, grad, stream=0):
     check(load().ce_softmax_xent(logits, labels, n, k, loss, grad, stream))
+
+
+def relu_fwd(x, count, precision, y, mask, stream=0):
+    check(load().ce_relu_fwd(x, count, PRECISIONS[precision], y, mask, stream))
+
+
+def relu_bwd(dy, mask, count, precision, dx, stream=0):
+    check(load().ce_relu_bwd(dy, mask, count, PRECISIONS[precision], dx, stream))
 
 
 def sgd_momentum(w, vel, g, count, lr, momentum, stream=0):
@@ -380,6 +391,20 @@ class Net:
                                        C.byref(by)))
             check(lib.ce_net_prof_ideal(self._h, cls, C.byref(ideal)))
             out[name.value.decode()] = (n.value, ms.value, fl.value, by.value, ideal.value)
+        return out
+
+    def profile_layers(self, n_layers):
+        """{(layer, class): (launches, ms, flops, bytes, ideal_ms)} for every layer (and -1) with launches."""
+        lib, out = load(), {}
+        names = [c for c in self.profile()]
+        for layer in range(-1, n_layers):
+            for cls, name in enumerate(names):
+                n = C.c_longlong()
+                ms, fl, by, ideal = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+                check(lib.ce_net_prof_layer(self._h, layer, cls, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by),
+                                            C.byref(ideal)))
+                if n.value:
+                    out[(layer, name)] = (n.value, ms.value, fl.value, by.value, ideal.value)
         return out
 
     def latency(self, x, warmup, reps):

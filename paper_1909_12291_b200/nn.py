@@ -85,6 +85,11 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def _precision_of(t):
+    """Kernel precision of a device tensor: bf16 stays bf16, everything else runs as float32."""
+    return "bf16" if t.dtype == torch.bfloat16 else "fp32"
+
+
 def _to_nhwc(x, c_store, dtype):
     """NCHW (possibly a view of NHWC storage) -> contiguous NHWC with channels
     zero-padded to c_store, in the kernel's activation type."""
@@ -286,12 +291,23 @@ class ReLU(Layer):
         return in_shape
 
     def forward(self, x):
-        x = _as_tensor(x)
-        self._mask = x > 0
-        return torch.where(self._mask, x, torch.zeros((), dtype=x.dtype, device=x.device))
+        x = _as_tensor(x).contiguous()
+        if x.dtype not in (torch.bfloat16, torch.float32):
+            x = x.float()
+        y = torch.empty_like(x)
+        self._mask = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+        native.relu_fwd(x.data_ptr(), x.numel(), _precision_of(x), y.data_ptr(), self._mask.data_ptr(), _stream())
+        return y
 
     def backward(self, grad_out):
-        return grad_out * self._mask
+        g = _as_tensor(grad_out).contiguous()
+        if g.dtype not in (torch.bfloat16, torch.float32):
+            g = g.float()
+        if g.shape != self._mask.shape:
+            raise ShapeError(f"relu backward: grad shape {tuple(g.shape)} != {tuple(self._mask.shape)}")
+        dx = torch.empty_like(g)
+        native.relu_bwd(g.data_ptr(), self._mask.data_ptr(), g.numel(), _precision_of(g), dx.data_ptr(), _stream())
+        return dx
 
 
 class Flatten(Layer):

@@ -265,3 +265,23 @@ def test_network_validation():
         nn.sgd_step(net, 0.0)
     with pytest.raises(ValueError):
         nn.Conv2d(3, 8, 0)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("shape", [(4, 8, 13, 13), (3, 5), (1, 7, 1, 1)])
+def test_relu_native_exact(dtype, shape):
+    """Operator-API ReLU runs the library kernel (ce_relu_fwd/bwd) and matches
+    nn.py:178-183 exactly: where(x > 0, x, 0) and grad * (x > 0)."""
+    rng = np.random.default_rng(len(shape))
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    x = torch.from_numpy(rng.standard_normal(shape).astype(np.float32)).to(tdt).cuda()
+    x.view(-1)[0] = 0.0  # x == 0 is not > 0
+    g = torch.from_numpy(rng.standard_normal(shape).astype(np.float32)).to(tdt).cuda()
+    layer = nn.ReLU()
+    y = layer.forward(x)
+    dx = layer.backward(g)
+    torch.cuda.synchronize()
+    xr = x.float().cpu().numpy()
+    np.testing.assert_array_equal(y.float().cpu().numpy(), np.where(xr > 0, xr, 0))
+    np.testing.assert_array_equal(dx.float().cpu().numpy(), g.float().cpu().numpy() * (xr > 0))
+    assert y.dtype == tdt and dx.dtype == tdt and layer._mask.dtype == torch.uint8

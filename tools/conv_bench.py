@@ -1,8 +1,11 @@
 """Conv pass microbenchmark through the kernel-level ABI (CUDA events on the
-launching stream, inputs larger than L2 or L2 flushed between reps).
+launching stream, L2 flushed between reps), with nvidia-smi clocks and
+throttle reasons sampled during the timed reps (bench.ClockSampler).
 
-    python tools/conv_bench.py [shape ...]     shape = n,c,h,co,k,s
-Default: the SWEET layer (256->256, k4, s1, 97x97 -> 94x94, B=64).
+    python tools/conv_bench.py [shape ...] [fwd|dgrad|wgrad] [vgg] [pool=k,s]
+        shape = n,c,h,co,k,s
+Default: the SWEET layer (256->256, k4, s1, 97x97 -> 94x94, B=64);
+`vgg` adds every VGG16STYLE conv layer with C_out >= 128 at B=64.
 """
 import json
 import sys
@@ -10,9 +13,13 @@ import sys
 import torch
 
 sys.path.insert(0, ".")
+from bench import ClockSampler  # noqa: E402
 from paper_1909_12291_b200 import native  # noqa: E402
 
 SWEET = (64, 256, 97, 256, 4, 1)
+# VGG16STYLE conv layers with C_out >= 128 at B=64: (n, c_in, h_in, c_out, k, s)
+VGG = [(64, 64, 48, 128, 3, 1), (64, 128, 46, 128, 3, 1), (64, 128, 22, 256, 3, 1), (64, 256, 20, 256, 3, 1),
+       (64, 256, 18, 256, 3, 1), (64, 256, 8, 256, 3, 1), (64, 256, 6, 256, 3, 1)]
 
 
 def bench_shape(shape, reps=10, passes=("fwd", "dgrad", "wgrad")):
@@ -59,7 +66,23 @@ def bench_shape(shape, reps=10, passes=("fwd", "dgrad", "wgrad")):
 
 
 if __name__ == "__main__":
-    shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:] if "," in a] or [SWEET]
-    only = [a for a in sys.argv[1:] if a in ("fwd", "dgrad", "wgrad")]
-    for sh in shapes:
-        print(json.dumps(bench_shape(sh, passes=tuple(only) or ("fwd", "dgrad", "wgrad"))), flush=True)
+    args = sys.argv[1:]
+    shapes = [tuple(int(v) for v in a.split(",")) for a in args if "," in a and "=" not in a]
+    if "vgg" in args:
+        shapes += VGG
+    shapes = shapes or [SWEET]
+    only = [a for a in args if a in ("fwd", "dgrad", "wgrad")]
+    reps = int(next((a.split("=")[1] for a in args if a.startswith("reps=")), 10))
+    # bring the SM clock up before the first timed shape (a cold GPU starts below max clocks)
+    a_ = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    for _ in range(60):
+        a_ @ a_
+    torch.cuda.synchronize()
+    del a_
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    rows = [bench_shape(sh, reps=reps, passes=tuple(only) or ("fwd", "dgrad", "wgrad")) for sh in shapes]
+    info = clocks.stop()
+    for r in rows:
+        r["clocks"] = info
+        print(json.dumps(r), flush=True)
