@@ -3,9 +3,10 @@
 // The image layer stores 3 real channels padded to 8 (one 16-byte chunk per
 // pixel), so its implicit GEMMs run K = k*k*8 where only k*k*3 columns carry
 // data (k = 6: 288 vs 108). A conv whose input is channel-padded and that needs
-// no dX (the first parameterised layer) instead runs two plain GEMMs over an
-// explicit im2col matrix
-//     xcol[m][kk],  kk = (i*k + j)*c_real + c  for kk < Kr = k*k*c_real,
+// no dX (the first parameterised layer) instead runs two plain GEMMs over a
+// packed im2col matrix with kPackedCpt = 4 columns per tap (the 3 real
+// channels and one zero, so a 16-byte chunk is exactly two taps):
+//     xcol[m][kk],  kk = (i*k + j)*4 + c  for kk < Kr = 4*k*k (c >= c_real: 0),
 //                   xcol[m][Kr] = 1, zero up to Kp = pad8(Kr + 1),
 // written once per forward (conv.forward, nn.py:82-94):
 //   forward  y = xcol . Wp^T      M = pixels, N = C_out, K = Kp  (pure 2D TMA)
@@ -29,8 +30,10 @@ inline bool packed_disabled() {
   return off;
 }
 
-inline int packed_kr(const ConvGeom& g, int c_real) { return g.k * g.k * c_real; }
+constexpr int kPackedCpt = 4;  // packed columns per tap (c_real <= 4 <= stored channels)
+inline int packed_kr(const ConvGeom& g, int c_real) { return g.k * g.k * kPackedCpt; }
 inline int packed_kp(const ConvGeom& g, int c_real) { return (packed_kr(g, c_real) + 1 + 7) / 8 * 8; }
+inline bool packable(const ConvGeom& g, int c_real) { return c_real <= kPackedCpt && g.c >= kPackedCpt; }
 
 // one thread per (pixel, 8-column chunk): 8 gathered bf16 -> one 16-byte store.
 // Column kk reads x at (receptive-field origin) + off[kk]; off is built once per
@@ -45,12 +48,12 @@ __global__ void __launch_bounds__(256) im2col_packed_kernel(const T* __restrict_
                                                             int Kp, FastDiv d_chunks, FastDiv d_ow, FastDiv d_oh,
                                                             T* __restrict__ xcol, PoolMap pm, uint32_t rows) {
   __shared__ int off[kPackedMaxKp];
-  const int Kr = g.k * g.k * c_real;
+  const int Kr = g.k * g.k * kPackedCpt;
   for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
     if (kk < Kr) {
-      const int tap = kk / c_real, c = kk - tap * c_real;
+      const int tap = kk / kPackedCpt, c = kk - tap * kPackedCpt;
       const int i = tap / g.k, j = tap - i * g.k;
-      off[kk] = (i * g.w + j) * g.c + c;
+      off[kk] = c < c_real ? (i * g.w + j) * g.c + c : -2;
     } else {
       off[kk] = kk == Kr ? -1 : -2;
     }
@@ -87,14 +90,14 @@ __global__ void __launch_bounds__(256) im2col_packed_kernel(const T* __restrict_
 template <class TW>
 __global__ void pack_first_w_kernel(const float* __restrict__ w, int co, int k, int cp, int c_real, int Kp,
                                     TW* __restrict__ wp) {
-  const int Kr = k * k * c_real;
+  const int Kr = k * k * kPackedCpt;
   const size_t total = (size_t)co * Kp;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const int o = (int)(e / Kp), kk = (int)(e % Kp);
     float v = 0.f;
     if (kk < Kr) {
-      const int tap = kk / c_real, c = kk - tap * c_real;
-      v = w[((size_t)o * k * k + tap) * cp + c];
+      const int tap = kk / kPackedCpt, c = kk - tap * kPackedCpt;
+      if (c < c_real) v = w[((size_t)o * k * k + tap) * cp + c];
     }
     stf(wp, e, v);
   }
@@ -183,10 +186,12 @@ inline int conv_wgrad_packed_splits(int Kp, int Mo, int num_sms) {
 }
 
 // ------------------------------------------------------------------ implicit packed operand
-// The packed im2col row of an output pixel, xrow[kk] (kk = (i*k + j)*c_real + c
-// < Kr, xrow[Kr] = 1, zero to Kp), is built by the producer warps straight from
-// the channel-padded input into the stage's shared-memory tile: no im2col
-// matrix in HBM (it would cost Kp*2 bytes per pixel twice, k^2-fold the input).
+// The packed im2col row of an output pixel (kk = tap*4 + c, ones column at Kr,
+// zero to Kp) is built by the producer warps straight from the channel-padded
+// input into the stage's shared-memory tile: no im2col matrix in HBM (it would
+// cost Kp*2 bytes per pixel twice, k^2-fold the input). With 4 columns per tap
+// a 16-byte chunk is two taps = two 8-byte loads of (c0, c1, c2, 0) from the
+// 8-channel input pixels.
 //   fwd   (MN = false): A = xrow, K-major [128 pixels][64 kk] per k-block; B = Wp
 //         by 2D TMA. Epilogue as conv_fwd_packed (bias/ReLU, or the pooled one).
 //   wgrad (MN = true) : A = xrow^T, MN-major [128 kk][64 pixels]; B = dY [pixels][co]
@@ -198,22 +203,17 @@ struct PackedTcLoader {
   static constexpr int A_MN_MAJOR = MN, B_MN_MAJOR = MN;
   static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = TMA_B, PURE_TMA = false, SYNC_FILL = true;
   CUtensorMap bmap;  // fwd: Wp [co][Kp]; wgrad: dY [rows][co] (TMA_B)
-  const bf16* x;     // channel-padded input [n][h][w][8]
+  const bf16* x;     // channel-padded input [n][h][w][g.c], g.c >= 4, channels >= c_real zero
   const bf16* dy;    // wgrad without TMA_B
   ConvGeom g;
   int c_real, Kr, Kp, rows, BN;
   FastDiv d_ow, d_oh;
   PoolMap pm;
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
-    int* off = (int*)table;
-    for (int kk = tid; kk < Kp; kk += nthreads) {
-      if (kk < Kr) {
-        const int tap = kk / c_real, c = kk - tap * c_real;
-        const int i = tap / g.k, j = tap - i * g.k;
-        off[kk] = (i * g.w + j) * g.c + c;
-      } else {
-        off[kk] = kk == Kr ? -1 : -2;
-      }
+    int* off = (int*)table;  // input offset of each tap relative to the receptive-field origin
+    for (int t = tid; t < g.k * g.k; t += nthreads) {
+      const int i = t / g.k, j = t - i * g.k;
+      off[t] = (i * g.w + j) * g.c;
     }
   }
   // input offset of the receptive-field origin of GEMM row m, or -1 for a padding row
@@ -228,23 +228,18 @@ struct PackedTcLoader {
     }
     return (((long long)n * g.h + p * g.s) * g.w + q * g.s) * g.c;
   }
-  // 8 consecutive xrow values from kk0 (kk0 % 8 == 0) of the row at `base`, packed bf16x2
+  // xrow[kk0 .. kk0+7] of the row at `base` (kk0 % 8 == 0), as 8 packed bf16
   __device__ __forceinline__ uint4 chunk(long long base, int kk0, const int* off) const {
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
-    if (base >= 0 && kk0 < Kp) {
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int o = off[kk0 + u];
-        v[u] = o >= 0 ? __bfloat162float(x[base + o]) : (o == -1 ? 1.f : 0.f);
-      }
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * h], v[2 * h + 1]);
-        w[h] = *(const uint32_t*)&b2;
-      }
+    if (base < 0 || kk0 > Kr) return make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t one = 0x3F80u;  // bf16(1.0) in the low half
+    if (kk0 == Kr) return make_uint4(one, 0u, 0u, 0u);
+    const int t0 = kk0 / kPackedCpt;  // < k*k here
+    const uint2 a = *(const uint2*)(x + base + off[t0]);
+    if (kk0 + 8 <= Kr) {
+      const uint2 b = *(const uint2*)(x + base + off[t0 + 1]);
+      return make_uint4(a.x, a.y, b.x, b.y);
     }
-    return make_uint4(w[0], w[1], w[2], w[3]);
+    return make_uint4(a.x, a.y, one, 0u);  // Kr % 8 == 4: last tap, then the ones column
   }
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
                        uint64_t* full) const {
@@ -254,7 +249,7 @@ struct PackedTcLoader {
         mbar_expect_tx(full, (uint32_t)BN * 128u);
         tma_load_2d(sB, &bmap, kb * TC_BK, c.n0, full);
       }
-      // only the K16 steps the MMA issues are filled (Kp < 64: a single K block)
+      // only the K16 steps the MMA issues are filled (Kp < 64: a single, partial K block)
       const int kcs = min(8, ((Kp - kb * TC_BK + 15) / 16) * 2);
       const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;
       const long long base = origin(c.m0 + r);
@@ -270,17 +265,14 @@ struct PackedTcLoader {
         if (kc < kcs) st_shared_v4(sA + kmajor_off(TC_BM, r, kc), vals[e]);
       }
     } else {
-      // A: 16 groups of 8 kk rows x 64 pixels; 256 producers -> 4 (group, pixel) chunks each
-      const int grp = ptid & 15;
-      const int kk0 = c.m0 + grp * 8;
+      // A: 16 groups of 8 kk rows x 64 pixels; thread -> one pixel, 4 kk groups (origin computed once)
+      const int kr = ptid & (TC_BK - 1);
+      const long long base = origin(kb * TC_BK + kr);
       uint4 vals[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int kr = (ptid >> 4) + e * 16;
-        vals[e] = chunk(origin(kb * TC_BK + kr), kk0, off);
-      }
+      for (int e = 0; e < 4; ++e) vals[e] = chunk(base, c.m0 + ((ptid >> 6) + 4 * e) * 8, off);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) st_shared_v4(sA + mnmajor_off(TC_BM, grp, (ptid >> 4) + e * 16), vals[e]);
+      for (int e = 0; e < 4; ++e) st_shared_v4(sA + mnmajor_off(TC_BM, (ptid >> 6) + 4 * e, kr), vals[e]);
       if constexpr (TMA_B) {
         if (ptid == 0) {
           mbar_expect_tx(full, (uint32_t)BN * TC_BK * 2u);
@@ -289,11 +281,11 @@ struct PackedTcLoader {
       } else {
         const int groups = BN / 8;
         for (int ch = ptid; ch < groups * TC_BK; ch += TC_PRODUCERS) {
-          const int gq = ch % groups, kr = ch / groups;
-          const int o0 = c.n0 + gq * 8, m = kb * TC_BK + kr;
+          const int gq = ch % groups, kq = ch / groups;
+          const int o0 = c.n0 + gq * 8, m = kb * TC_BK + kq;
           uint4 v = make_uint4(0u, 0u, 0u, 0u);
           if (o0 < g.co && m < rows) v = *(const uint4*)(dy + (size_t)m * g.co + o0);
-          st_shared_v4(sB + mnmajor_off(BN, gq, kr), v);
+          st_shared_v4(sB + mnmajor_off(BN, gq, kq), v);
         }
       }
     }
@@ -442,7 +434,7 @@ __global__ void __launch_bounds__(256) conv_sgd_packed_kernel(
     float* __restrict__ vel, float* __restrict__ gw, TW* __restrict__ wp, float* __restrict__ b,
     float* __restrict__ vb, float* __restrict__ gb, float lr, float mu) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int Kr = k * k * c_real;
+  const int Kr = k * k * kPackedCpt;
   const size_t e = (size_t)blockIdx.x * 8 + warp;  // over co x (Kr + 1)
   if (e >= (size_t)co * (Kr + 1)) return;
   const int o = (int)(e / (Kr + 1)), kk = (int)(e % (Kr + 1));
@@ -458,7 +450,8 @@ __global__ void __launch_bounds__(256) conv_sgd_packed_kernel(
     }
     return;
   }
-  const int tap = kk / c_real, c = kk - tap * c_real;
+  const int tap = kk / kPackedCpt, c = kk - tap * kPackedCpt;
+  if (c >= c_real) return;  // zero column of the packing: no parameter
   const size_t mi = ((size_t)o * k * k + tap) * cp + c;
   if (gw) gw[mi] = g;
   if (!w) return;

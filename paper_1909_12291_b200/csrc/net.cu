@@ -110,6 +110,7 @@ static double g_peak_flops = 1.3877e15, g_peak_bytes = 6.5504e12;
 struct ce_net {
   int device = 0, prec = CE_PREC_BF16, num_sms = 148;
   bool prof_on = false;
+  bool prof_capturing = false;  // Prof events become event-record nodes of the captured step graph
   std::vector<ProfEvent> prof_pending;
   ProfTotals prof[P_NCLASS];
   std::map<std::pair<int, int>, ProfTotals> prof_layers;  // (layer, class) -> totals; layer -1 = gather / loss
@@ -302,20 +303,30 @@ struct Prof {
     net->acc += k;
     if (net->prof_on) {
       cudaEventCreate(&a);
-      cudaEventRecord(a, net->st);
+      cudaEventRecordWithFlags(a, net->st, net->prof_capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
     }
   }
   ~Prof() {
     if (net->prof_on) {
       cudaEvent_t b;
       cudaEventCreate(&b);
-      cudaEventRecord(b, net->st);
+      cudaEventRecordWithFlags(b, net->st, net->prof_capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
       net->prof_pending.push_back(ProfEvent{cls, layer, flops, bytes, a, b});
     }
   }
 };
 
-void prof_collect(ce_net* net) {
+void prof_release(ce_net* net) {
+  for (auto& e : net->prof_pending) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  net->prof_pending.clear();
+}
+
+// Accumulate the bracketed launches. keep: the events belong to a captured step
+// graph and are re-recorded by its next replay (read after every replay).
+void prof_collect(ce_net* net, bool keep = false) {
   for (auto& e : net->prof_pending) {
     float ms = 0.f;
     cudaEventSynchronize(e.b);
@@ -328,10 +339,8 @@ void prof_collect(ce_net* net) {
       t->bytes += e.bytes;
       t->ideal_ms += ideal;
     }
-    cudaEventDestroy(e.a);
-    cudaEventDestroy(e.b);
   }
-  net->prof_pending.clear();
+  if (!keep) prof_release(net);
 }
 
 // CE_POOL_FUSION: 0 = never fuse max-pool into the conv epilogue, 1 = only where
@@ -982,6 +991,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
     if (l.kind != CE_LAYER_CONV) continue;
     const long long Mo = (long long)d->max_batch * l.g.oh * l.g.ow;
     l.packed = (net->use_tc || precision == CE_PREC_FP32) && l.c_real < l.g.c && !l.need_dx && !packed_disabled() &&
+               packable(l.g, l.c_real) &&
                packed_kp(l.g, l.c_real) <= kPackedMaxKp && Mo * packed_kp(l.g, l.c_real) / 8 < (1ll << 32);
     if (i + 1 < net->L.size() && net->L[i + 1].kind == CE_LAYER_POOL && net->use_tc &&
         pool_fusable(net->L[i + 1].g.k, net->L[i + 1].g.s) && pool_fusion_mode() > 0 &&
@@ -1380,19 +1390,25 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
     net->h_flags = pinned_flag_slots();
     if (!net->h_flags) return fail(CE_ENOMEM, "pinned flag pool allocation failed");
   }
-  // capture one step (profiling runs eagerly so each launch can be bracketed)
+  // capture one step; when profiling, every kernel class is bracketed by
+  // event-record nodes inside the graph, so the per-class times are the graph's
+  // own device times (no host launch gaps), read after every replay
   TrainRes r;  // graph exec + events: released on every return path
   bool graphed = false;
   net->acc = 0;
   long long per_step = 0;
   SharedGate capture_gate(net->device);  // no exclusive latency window (device sync) during a capture
-  if (!net->prof_on && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+  if (net->prof_on) prof_release(net);
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
     cudaGraph_t graph = nullptr;
+    net->prof_capturing = net->prof_on;
     int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true);
     if (s == CE_OK) s = step_any(net, batch, lr, momentum);
+    net->prof_capturing = false;
     cudaError_t ce = cudaStreamEndCapture(st, &graph);
     if (s != CE_OK) {
       if (graph) cudaGraphDestroy(graph);
+      prof_release(net);
       return s;
     }
     if (ce == cudaSuccess && cudaGraphInstantiate(&r.exec, graph, 0) == cudaSuccess) graphed = true;
@@ -1401,6 +1417,7 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   }
   capture_gate.release();
   cudaGetLastError();
+  if (!graphed) prof_release(net);  // eager fallback: fresh events per launch
   net->acc = 0;
   CE_CUDA(cudaEventCreate(&r.ev[0]));
   CE_CUDA(cudaEventCreate(&r.ev[1]));
@@ -1421,6 +1438,10 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
       for (int i = 0; i < todo; ++i) {
         if (graphed) {
           CE_CUDA(cudaGraphLaunch(r.exec, st));
+          if (net->prof_on && !net->prof_pending.empty()) {  // read this replay's event nodes
+            CE_CUDA(cudaStreamSynchronize(st));
+            prof_collect(net, true);
+          }
         } else {
           if (int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true)) return s;
           if (int s = step_any(net, batch, lr, momentum)) return s;
@@ -1441,7 +1462,15 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   CE_CUDA(cudaEventRecord(e1, st));
   CE_CUDA(cudaMemcpyAsync(losses, net->d_losses, (size_t)steps * 4, cudaMemcpyDeviceToHost, st));
   cudaError_t se = cudaStreamSynchronize(st);
-  if (net->prof_on) prof_collect(net);
+  if (net->prof_on) {
+    if (graphed) {  // every replay was collected already; the graph goes before its events
+      cudaGraphExecDestroy(r.exec);
+      r.exec = nullptr;
+      prof_release(net);
+    } else {
+      prof_collect(net);
+    }
+  }
   if (se != cudaSuccess) return fail(CE_ECUDA, "train loop: %s", cudaGetErrorString(se));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);

@@ -157,30 +157,67 @@ def test_t4_evaluate_fixed_3steps(splits, precision):
         print(f"FIXED 3 steps bf16: scores rel {rel(scores, ref_scores):.3e}, near-ties {edge:.2f}")
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16"])
-def test_t4_c1_full_budget(splits, precision):
-    """The whole C1 candidate (2 epochs x 62 steps at B=64) vs convevo's own run."""
-    gold = _golden("candidate.json").get("c1_fixed_full")
-    if gold is None:
-        pytest.skip("c1 golden not generated")
+def _c1_ensemble(splits, precision, variants):
+    """The C1 candidate (FIXED, B=64, 2 epochs) through ce_train + ce_predict with every
+    batch's samples in an order shuffled by default_rng(s) (s = 0: reference order): the
+    same math, a different float summation order (tools/c1_ensemble.py)."""
+    from paper_1909_12291_b200.candidate import DATASETS, epoch_permutations
+    from paper_1909_12291_b200.scoring import auc_roc, confusion_counts
     genome = parse_genome(FIXED)
-    rec = evaluate(genome, splits, TrainBudget(epochs=2), FLOP_OBJ, seed=0, precision=precision)
-    assert rec.ok == gold["ok"]
-    assert rec.flops_inference == gold["flops_inference"] and rec.params == gold["params"]
-    conf = rec.extras["confusion"]
-    if precision == "fp32":
-        _check_counts(conf, gold["confusion"], f"C1 {precision}")
-        assert abs(rec.val_auc - gold["val_auc"]) <= AUC_TOL, (rec.val_auc, gold["val_auc"])
-    else:
-        net, _ = train_short(genome, splits.train, TrainBudget(epochs=2), seed=0, precision="bf16")
+    n, bs = len(splits.train), genome.learn.batch_size
+    ds_tr, ds_val = DATASETS.get(splits.train, 0), DATASETS.get(splits.val, 0)
+    rows = []
+    for s in range(variants):
+        perms = epoch_permutations(0, n, 2)
+        if s:
+            rng = np.random.default_rng(s)
+            for e in range(2):
+                for start in range(0, n - bs + 1, bs):
+                    perms[e, start:start + bs] = perms[e, start:start + bs][rng.permutation(bs)]
+        net = instantiate(genome, splits.train.input_shape, seed=0)
+        dev = net.to_device(0, precision, max_batch=128)
         try:
-            scores, preds = predict_scores(net, splits.val)
+            losses, _ = dev.train(ds_tr, perms, n // bs, bs, genome.learn.lr, genome.learn.momentum)
+            scores, preds = dev.predict(ds_val, 128)
         finally:
             net.release()
-        _check_bf16_decisions(scores, preds, gold["scores"], gold["preds"], splits.val.labels, gold["val_auc"],
-                              rec.val_auc, "C1 bf16")
-    print(f"C1 {precision}: F1 {rec.val_f1:.4f} (ref {gold['val_f1']:.4f}) AUC {rec.val_auc:.4f} "
-          f"(ref {gold['val_auc']:.4f}) conf {conf} (ref {gold['confusion']})")
+        assert np.isfinite(losses).all()
+        rows.append((confusion_counts(preds, splits.val.labels), auc_roc(scores, splits.val.labels)))
+    return rows
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_t4_c1_outcome_distribution(splits, precision):
+    """The whole C1 candidate (2 epochs x 62 steps at B=64) vs the reference's own outcome.
+
+    At full budget the FIXED trajectory is chaotic: a change of float summation
+    order alone (reversed / shuffled batch order, reversed conv taps, float64)
+    moves the reference's own val tp over 2..13 and its AUC over 0.86..0.93
+    (tests/golden/c1_sensitivity.json, written by tools/c1_sensitivity.py from the
+    numpy oracle, whose reference-order run reproduces convevo's every loss), so
+    no implementation can be held to one run's counts. T4 is therefore applied
+    to the distributions: 16 summation-order variants of the product path
+    (ce_train + ce_predict) against the reference's variants. fp32 check mode:
+    medians of tp / fp / fn within COUNT_TOL, mean AUC within AUC_TOL, and a
+    Mann-Whitney U test on tp that does not separate them (p > 0.01). bf16: the
+    threshold-free AUC within AUC_TOL (bf16 storage shifts the knife-edge 0.5
+    decisions, which is reported)."""
+    sens = _golden("c1_sensitivity.json")
+    ref = list(sens["variants"].values())
+    ours = _c1_ensemble(splits, precision, 16)
+    ref_auc = np.mean([v["auc"] for v in ref])
+    our_auc = np.mean([a for _, a in ours])
+    med = {k: (float(np.median([c[k] for c, _ in ours])), float(np.median([v["confusion"][k] for v in ref])))
+           for k in ("tp", "fp", "fn")}
+    print(f"C1 {precision}: medians ours/ref {med}, mean AUC {our_auc:.4f} / {ref_auc:.4f}, "
+          f"tp ours {[c['tp'] for c, _ in ours]} ref {[v['confusion']['tp'] for v in ref]}")
+    assert abs(our_auc - ref_auc) <= AUC_TOL, (our_auc, ref_auc)
+    if precision == "fp32":
+        for k, (a, b) in med.items():
+            assert abs(a - b) <= COUNT_TOL, f"median {k}: {a} vs reference {b}"
+        from scipy.stats import mannwhitneyu
+        p = mannwhitneyu([c["tp"] for c, _ in ours], [v["confusion"]["tp"] for v in ref]).pvalue
+        assert p > 0.01, f"tp distributions separate (Mann-Whitney p = {p:.4f})"
 
 
 def _c2_rows():
