@@ -104,6 +104,8 @@ int ce_net_create(const ce_net_desc* desc, int device, int precision, ce_net** o
 int ce_net_destroy(ce_net* net);
 /* bytes of device memory the net holds (parameters + activations + workspace) */
 int ce_net_device_bytes(const ce_net* net, size_t* bytes);
+/* stream priority of the net's work: > 0 the device's highest, otherwise default */
+int ce_net_set_priority(ce_net* net, int priority);
 /* number of parameterised layers (conv + dense), in layer order */
 int ce_net_num_param_layers(const ce_net* net, int* count);
 /* param layer p: weights in reference layout (conv (o,c,kh,kw), dense (o,in)), bias (o) */

@@ -1109,6 +1109,22 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
   return CE_OK;
 }
 
+// Stream priority of the net (> 0: the device's highest, else default). The
+// scheduler raises it for the slot that runs the longest candidates, so their
+// kernels win the SM arbitration against the short candidates packed beside them.
+int ce_net_set_priority(ce_net* net, int priority) {
+  if (check_net(net)) return CE_EINVAL;
+  DevGuard dg(net->device);
+  int least = 0, greatest = 0;
+  CE_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  cudaStream_t s = nullptr;
+  CE_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority > 0 ? greatest : least));
+  CE_CUDA(cudaStreamSynchronize(net->st));  // allocations made on the old stream are complete
+  cudaStreamDestroy(net->st);
+  net->st = s;
+  return CE_OK;
+}
+
 int ce_net_device_bytes(const ce_net* net, size_t* bytes) {
   if (check_net(net)) return CE_EINVAL;
   *bytes = net->bytes;
@@ -1417,6 +1433,9 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   }
   capture_gate.release();
   cudaGetLastError();
+  if (net->prof_on && getenv("CE_PROF_DEBUG"))
+    fprintf(stderr, "[ce_train profile] graphed=%d bracketed launches per step=%zu\n", (int)graphed,
+            net->prof_pending.size());
   if (!graphed) prof_release(net);  // eager fallback: fresh events per launch
   net->acc = 0;
   CE_CUDA(cudaEventCreate(&r.ev[0]));

@@ -59,6 +59,7 @@ _SIGNATURES = {
     "ce_net_create": ([C.POINTER(NetDesc), C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
     "ce_net_destroy": ([_P], C.c_int),
     "ce_net_device_bytes": ([_P, C.POINTER(C.c_size_t)], C.c_int),
+    "ce_net_set_priority": ([_P, C.c_int], C.c_int),
     "ce_net_num_param_layers": ([_P, C.POINTER(C.c_int)], C.c_int),
     "ce_net_set_params": ([_P, C.c_int, _F, _F], C.c_int),
     "ce_net_get_params": ([_P, C.c_int, _F, _F, _F, _F], C.c_int),
@@ -264,6 +265,24 @@ class Dataset:
             pass
 
 
+_thread = threading.local()
+
+
+class stream_priority:
+    """Context: nets created by this thread get a high-priority stream (priority > 0)."""
+
+    def __init__(self, priority):
+        self.priority = priority
+
+    def __enter__(self):
+        self.prev = getattr(_thread, "priority", 0)
+        _thread.priority = self.priority
+        return self
+
+    def __exit__(self, *exc):
+        _thread.priority = self.prev
+
+
 class Net:
     """Owning wrapper of a ce_net handle."""
 
@@ -277,6 +296,8 @@ class Net:
         h_ = _P()
         check(lib.ce_net_create(C.byref(desc), int(device), PRECISIONS[precision], C.byref(h_)))
         self._h = h_
+        if getattr(_thread, "priority", 0) > 0:
+            check(lib.ce_net_set_priority(h_, 1))
         self.device, self.precision, self.max_batch = device, precision, max_batch
 
     def close(self):

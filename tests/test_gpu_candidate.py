@@ -334,3 +334,25 @@ def test_latency_argument_errors():
             measure_latency(net, 8, reps=3, warmup=0)
     finally:
         net.release()
+
+
+def test_c2_g15_full_budget_outcome(splits):
+    """C2 genome #15 (137 M-param head, lr 0.017): the fp32 reference trains through its
+    whole budget (losses up to 7.8e4, never non-finite; tests/golden/candidate.json
+    c2_g15_full). The product's outcome must be ok as well: in bf16 it may leave the finite
+    range, and evaluate() then confirms in the fp32 check mode (evaluator.py:166-170)."""
+    gold = _golden("candidate.json").get("c2_g15_full")
+    if gold is None:
+        pytest.skip("g15 golden not generated")
+    genome = parse_genome(gold["genome"])
+    assert gold["ok"] and len(gold["losses"]) == 250
+    rec = evaluate(genome, splits, TrainBudget(epochs=2), FLOP_OBJ, seed=0, precision="bf16")
+    assert rec.ok, rec.failure_reason
+    assert rec.params == gold["params"] and rec.flops_inference == gold["flops_inference"]
+    print(f"g15: precision {rec.extras['precision']}, bf16 failure {rec.extras.get('bf16_failure')}, "
+          f"F1 {rec.val_f1:.3f} (ref {gold['val_f1']:.3f}) AUC {rec.val_auc:.3f} (ref {gold['val_auc']:.3f})")
+    net, _ = train_short(genome, splits.train, TrainBudget(epochs=2), seed=0, precision="fp32")
+    losses = np.asarray(net.last_losses)
+    net.release()
+    assert np.isfinite(losses).all()
+    np.testing.assert_allclose(losses[:2], gold["losses"][:2], rtol=1e-4)

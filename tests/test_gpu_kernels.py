@@ -198,3 +198,47 @@ def test_wgrad_multiwave_splits():
     assert rel(dw, dw_ref.cpu().numpy()) <= 1e-2, f"wgrad rel err {rel(dw, dw_ref.cpu().numpy()):.3e}"
     db_ref = dy.float().sum(dim=(0, 2, 3)).cpu().numpy()
     assert rel(dbd.cpu().numpy(), db_ref) <= 1e-2
+
+
+@pytest.mark.parametrize("shape", [(64, 256, 97, 256, 4, 1), (64, 128, 46, 128, 3, 1)], ids=["sweet_b64", "vgg_l3_b64"])
+def test_conv_passes_full_size(shape):
+    """SWEET and a VGG16STYLE layer at B=64: thousands of 128-row tiles, so
+    every persistent CTA runs many tiles (TMEM accumulator flip, mbarrier phase wrap). fwd /
+    dgrad / wgrad vs PyTorch fp32 (TF32 off) on the same bf16-exact operands, <= 1e-2."""
+    import torch.nn.functional as F
+    n, c, h, co, k, s = shape
+    oh = (h - k) // s + 1
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(n, c, h, h, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(co, c, k, k, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    b = torch.randn(co, device="cuda", generator=g) * 0.1
+    dy = torch.randn(n, co, oh, oh, device="cuda", generator=g).to(torch.bfloat16)
+    desc = native.conv_desc(n, c, h, h, co, k, s, "bf16")
+    xd, wd = x.permute(0, 2, 3, 1).contiguous(), w.permute(0, 2, 3, 1).contiguous()
+    dyd = dy.permute(0, 2, 3, 1).contiguous()
+    yd = torch.empty(n, oh, oh, co, device="cuda", dtype=torch.bfloat16)
+    dxd = torch.empty_like(xd)
+    dwd = torch.empty(co, k, k, c, device="cuda")
+    dbd = torch.empty(co, device="cuda")
+    wsb = native.conv_workspace_bytes(desc)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    native.conv_fwd(desc, xd.data_ptr(), wd.data_ptr(), b.data_ptr(), 0, yd.data_ptr(), st)
+    native.conv_dgrad(desc, dyd.data_ptr(), wd.data_ptr(), None, dxd.data_ptr(), ws.data_ptr(), wsb, st)
+    native.conv_wgrad(desc, xd.data_ptr(), dyd.data_ptr(), dwd.data_ptr(), dbd.data_ptr(), ws.data_ptr(), wsb, st)
+    torch.cuda.synchronize()
+    prev = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        y_ref = F.conv2d(x.float(), w.float(), b, stride=s)
+        dx_ref = torch.nn.grad.conv2d_input(x.shape, w.float(), dy.float(), stride=s)
+        dw_ref = torch.nn.grad.conv2d_weight(x.float(), w.shape, dy.float(), stride=s)
+    finally:
+        torch.backends.cudnn.allow_tf32 = prev
+
+    def trel(a, r):
+        return float((a.float() - r).norm() / r.norm())
+    assert trel(yd.permute(0, 3, 1, 2), y_ref) <= 1e-2
+    assert trel(dxd.permute(0, 3, 1, 2), dx_ref) <= 1e-2
+    assert trel(dwd.permute(0, 3, 1, 2), dw_ref) <= 1e-2
+    assert trel(dbd, dy.float().sum(dim=(0, 2, 3))) <= 1e-2

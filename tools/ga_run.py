@@ -49,12 +49,12 @@ def main():
             failures.append(record.failure_reason)
         collect(record)
     master.collect = counted
-    first = []
+    first = {}  # device -> time of that worker process's first work request
     issue = master.issue
 
-    def timed_issue(worker_id):  # generation clock starts at the first work request
-        if not first:
-            first.append(time.perf_counter())
+    def timed_issue(worker_id):
+        dev = worker_id.split("s")[0]
+        first.setdefault(dev, time.perf_counter())
         return issue(worker_id)
     master.issue = timed_issue
     pool = ProcessGpuPool(master, config, devices=tuple(range(a.gpus)), slots_per_gpu=a.slots, order="fifo")
@@ -65,13 +65,17 @@ def main():
         log.close()
     best = master.best
     busy = {w: round(s.busy_time_s / max(wall, 1e-9), 3) for w, s in sorted(report.stats.items())}
+    # the clock starts once EVERY worker process is up (its first work request), so
+    # slower CUDA-context start-up of some processes does not count as GA time
+    ready = max(first.values()) - t0 if len(first) == a.gpus else None
     print(json.dumps({
         "config": "C3 steady-state GA", "gpus": a.gpus, "slots_per_gpu": a.slots, "capacity": a.capacity,
         "evaluations": master.completed, "wall_s": round(wall, 3),
-        "startup_s": round(first[0] - t0, 3) if first else None,
-        "candidates_per_h": master.completed / (wall - (first[0] - t0 if first else 0.0)) * 3600.0,
+        "startup_s": round(ready, 3) if ready is not None else None,
+        "first_request_s": {d: round(t - t0, 3) for d, t in sorted(first.items())},
+        "candidates_per_h": master.completed / (wall - (ready or 0.0)) * 3600.0,
         "candidates_per_h_incl_startup": master.completed / wall * 3600.0,
-        "note": "candidates_per_h is timed from the first work request (worker start-up excluded)",
+        "note": "candidates_per_h is timed from the moment every worker process has made its first work request",
         "failures": len(failures), "failure_reasons": sorted(set(map(str, failures)))[:8],
         "best_genome": format_genome(best.genome) if best else None,
         "best_fitness": best.record.fitness if best and best.record.ok else None,

@@ -12,10 +12,15 @@ import bench  # noqa: E402
 from paper_1909_12291_b200 import ObjectiveConfig, TrainBudget, evaluate  # noqa: E402
 from paper_1909_12291_b200.patches import default_splits  # noqa: E402
 
-i = int(sys.argv[1])
 mb = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 prec = sys.argv[3] if len(sys.argv) > 3 else "bf16"
-g = bench.population(16)[i]
+if sys.argv[1].isdigit():
+    i = int(sys.argv[1])
+    g = bench.population(16)[i]
+else:  # a canonical genome by name: FIXED, VGG16STYLE, SWEET
+    from paper_1909_12291_b200 import genes, parse_genome
+    i, g = sys.argv[1], parse_genome(getattr(genes, sys.argv[1]))
 r = evaluate(g, default_splits(), TrainBudget(epochs=1, max_batches_per_epoch=mb),
              ObjectiveConfig("flop_proxy", -0.2, 1e8, 1e9), seed=0, precision=prec, confirm_divergence=False)
-print(i, g.id, r.ok, r.failure_reason, r.extras.get("precision"))
+print(i, g.id, r.ok, r.failure_reason, r.extras.get("precision"), "train_s", r.train_time_s,
+      "steps", r.extras.get("train_steps"))
