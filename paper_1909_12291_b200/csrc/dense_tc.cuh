@@ -184,6 +184,103 @@ struct DenseDwSgdEpi {
   __device__ void finish(int, int) const {}
 };
 
+// ------------------------------------------------------------------ fp32 check mode on tensor cores
+// v -> three bf16 (hi, mid, lo) with v - (hi + mid + lo) below 2^-24 |v|
+__device__ __forceinline__ void split3(float v, bf16& hi, bf16& mid, bf16& lo) {
+  hi = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+// 4 consecutive fp32 values -> 8 bytes in each of the 3 planes at byte offset `off` of plane 0
+__device__ __forceinline__ void store_split4(uint32_t plane0, uint32_t plane_bytes, uint32_t off, float4 v) {
+  bf16 h[4], m[4], l[4];
+  split3(v.x, h[0], m[0], l[0]);
+  split3(v.y, h[1], m[1], l[1]);
+  split3(v.z, h[2], m[2], l[2]);
+  split3(v.w, h[3], m[3], l[3]);
+  const uint2 uh = *(const uint2*)h, um = *(const uint2*)m, ul = *(const uint2*)l;
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(plane0 + off), "r"(uh.x), "r"(uh.y) : "memory");
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(plane0 + plane_bytes + off), "r"(um.x), "r"(um.y) : "memory");
+  asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(plane0 + 2 * plane_bytes + off), "r"(ul.x), "r"(ul.y)
+               : "memory");
+}
+// 4 fp32 from row `row` (row stride ld), columns k..k+3 (< kmax), zero-filled
+__device__ __forceinline__ float4 ld4_guard(const float* base, size_t ld, int row, int rows, int k, int kmax) {
+  if (row >= rows || k >= kmax) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* p = base + (size_t)row * ld + k;
+  if (k + 3 < kmax && ((ld & 3) == 0)) return *(const float4*)p;
+  return make_float4(p[0], k + 1 < kmax ? p[1] : 0.f, k + 2 < kmax ? p[2] : 0.f, k + 3 < kmax ? p[3] : 0.f);
+}
+
+// fp32 dense forward part[split][b][o] = sum_k x[b][k] W[o][k] (nn.py:225-231) on the
+// tensor cores: A = W rows (outputs, K-major), B = x rows (batch, K-major), both split
+// into bf16 planes by the producers (Split3 in tc_engine.cuh).
+struct DenseSplitFwdLoader {
+  static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false, PURE_TMA = false, SYNC_FILL = true, SPLIT3 = true;
+  const float* w;  // [out][in]
+  const float* x;  // [B][x_ld]
+  int in, out, B, x_ld, BN;
+  __device__ void init(uint8_t*, int, int) const {}
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
+                       uint64_t*) const {
+    const int kq = ptid & 15, k = kb * TC_BK + 4 * kq;
+    const uint32_t off_k = kmajor_off(TC_BM, 0, kq >> 1) + (kq & 1) * 8;
+    float4 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = ld4_guard(w, (size_t)in, c.m0 + (ptid >> 4) + 16 * i, out, k, in);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      store_split4(sA, TC_BM * TC_BK * 2, off_k + (uint32_t)((ptid >> 4) + 16 * i) * 16u, v[i]);
+    const uint32_t offb_k = kmajor_off(BN, 0, kq >> 1) + (kq & 1) * 8;
+    for (int r = ptid >> 4; r < BN; r += 16)
+      store_split4(sB, BN * TC_BK * 2, offb_k + (uint32_t)r * 16u, ld4_guard(x, (size_t)x_ld, c.n0 + r, B, k, in));
+  }
+};
+
+// fp32 dense dX[b][i] = sum_o g[b][o] W[o][i] (pre-update W, nn.py:240): A = W^T
+// (MN-major: rows i contiguous in W's rows), B = g rows (K-major over o).
+struct DenseSplitDxLoader {
+  static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 0;
+  static constexpr bool A_TMA_SW128 = false, B_TMA_SW128 = false, PURE_TMA = false, SYNC_FILL = true, SPLIT3 = true;
+  const float* w;  // [out][in]
+  const float* g;  // [B][out]
+  int in, out, B, BN;
+  __device__ void init(uint8_t*, int, int) const {}
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
+                       uint64_t*) const {
+    // A: 64 output rows (K) x 128 inputs (MN); thread -> row ptid/4, inputs (ptid%4)*32 .. +31
+    const int kr = ptid >> 2, o = kb * TC_BK + kr, iq = (ptid & 3) * 32;
+    float4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = ld4_guard(w, (size_t)in, o, out, c.m0 + iq + 4 * j, in);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = iq + 4 * j;  // tile-local input index
+      store_split4(sA, TC_BM * TC_BK * 2, mnmajor_off(TC_BM, i >> 3, kr) + (i & 4) * 2, v[j]);
+    }
+    const int kq = ptid & 15, k = kb * TC_BK + 4 * kq;
+    const uint32_t offb_k = kmajor_off(BN, 0, kq >> 1) + (kq & 1) * 8;
+    for (int r = ptid >> 4; r < BN; r += 16)
+      store_split4(sB, BN * TC_BK * 2, offb_k + (uint32_t)r * 16u, ld4_guard(g, (size_t)out, c.n0 + r, B, k, out));
+  }
+};
+
+// CE_DENSE_SPLIT3=1 sends fp32 check-mode dense layers (>= 1 M parameters, B <= 64:
+// two accumulators x BN columns double-buffered must fit TMEM) to the split-plane
+// tensor-core GEMMs. Off by default: the producers' synchronous fp32 loads and
+// plane splits make it slower than the CUDA-core kernels on the C2 heads measured
+// (C2 #15, 262144 -> 523 at B = 32: forward 472 vs 335 us, profiles/r02_notes.md).
+constexpr long long kDenseSplitMinParams = 1ll << 20;
+inline bool dense_split3_enabled(int B, long long params) {
+  static const bool on = [] {
+    const char* e = getenv("CE_DENSE_SPLIT3");
+    return e && e[0] == '1';
+  }();
+  return on && B <= 64 && params >= kDenseSplitMinParams;
+}
+
 // ------------------------------------------------------------------ launchers
 inline int dense_fwd_splits(int out, int in, int num_sms) {
   const int m_tiles = (out + TC_BM - 1) / TC_BM;
@@ -208,6 +305,41 @@ inline int dense_fwd_tc(const bf16* x, int x_stride, const bf16* wb, int in, int
     DenseFwdEpi ep{part, out, B};
     cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "dense_fwd_tc: %s", cudaGetErrorString(e));
+  });
+}
+
+// fp32 dense forward on the tensor cores (split planes); returns the partial split count
+// tensor-core accumulation is not round-to-nearest: the fp32-check-mode forward keeps
+// every split's TMEM chain at <= kSplit3MaxKb K blocks and reduces the splits in IEEE fp32
+constexpr int kSplit3MaxKb = 8;
+inline int dense_fwd_split3_splits(int out, int in, int num_sms) {
+  const int nkb = (in + TC_BK - 1) / TC_BK;
+  return std::max(dense_fwd_splits(out, in, num_sms), (nkb + kSplit3MaxKb - 1) / kSplit3MaxKb);
+}
+
+inline int dense_fwd_split3(const float* x, int x_ld, const float* w, int in, int out, int B, float* part,
+                            int* splits_out, int num_sms, cudaStream_t st) {
+  return with_bn(B, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(out, B, in, BN, dense_fwd_split3_splits(out, in, num_sms));
+    *splits_out = sh.splits;
+    DenseSplitFwdLoader ld{w, x, in, out, B, x_ld, BN};
+    DenseFwdEpi ep{part, out, B};
+    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "dense_fwd_split3: %s", cudaGetErrorString(e));
+  });
+}
+
+template <class TM>
+inline int dense_dx_split3(const float* g, const float* w, int B, int in, int out, const TM* mask, float* dx,
+                           int num_sms, cudaStream_t st) {
+  return with_bn(B, [&](auto bn) {
+    constexpr int BN = decltype(bn)::value;
+    TcShape sh = tc_make_shape(in, B, out, BN, 1);
+    DenseSplitDxLoader ld{w, g, in, out, B, BN};
+    DenseDxEpiTc<float, TM> ep{dx, mask, in, B};
+    cudaError_t e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+    return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "dense_dx_split3: %s", cudaGetErrorString(e));
   });
 }
 

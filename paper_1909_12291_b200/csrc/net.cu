@@ -473,6 +473,9 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
         }
         int s = dense_fwd_tc(x16, l.in_pad, l.Wbp, K, l.in_pad, O, B, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
+      } else if (dense_split3_enabled(B, (long long)K * O)) {  // fp32 check mode on the tensor cores
+        int s = dense_fwd_split3((const float*)in, K, l.W, K, O, B, net->ws, &splits, net->num_sms, st);
+        if (s != CE_OK) return s;
       } else if (dense_fwd_simt_enabled()) {
         splits = dense_fwd_simt_splits(B, K, O, net->num_sms);
         while (splits > 1 && (size_t)splits * B * O * 4 > net->ws_bytes) --splits;
@@ -569,6 +572,15 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
       } else {
       const bool small = B <= kDenseSimtMaxBatch;
       if (l.need_dx) {
+        if constexpr (std::is_same<T, float>::value) {
+          if (dense_split3_enabled(B, (long long)K * O)) {  // fp32 check mode on the tensor cores
+            int s = l.in_is_act ? dense_dx_split3(g, l.W, B, K, O, mask, (float*)gout, net->num_sms, st)
+                                : dense_dx_split3(g, l.W, B, K, O, (const float*)nullptr, (float*)gout,
+                                                  net->num_sms, st);
+            if (s != CE_OK) return s;
+            goto dx_done;
+          }
+        }
         if (small) {
           if (l.in_is_act)
             dense_dx_simt(g, l.W, B, K, O, mask, (T*)gout, st);
@@ -580,6 +592,7 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
           simt_gemm(DenseGA{g, O}, DenseWN{l.W, K}, DenseDxEpi<float, float>{(float*)gout, nullptr, K}, B, K, O, 1,
                     st);
         }
+      dx_done:
         CE_CHECK_LAUNCH();
       }
       if (small) {
@@ -1030,6 +1043,8 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         int spt = dense_fwd_splits(l.out_units, l.in_units, net->num_sms);
         ws = std::max(ws, (size_t)spt * B * l.out_units * 4);
       }
+      if (precision == CE_PREC_FP32 && dense_split3_enabled(1, (long long)l.in_units * l.out_units))
+        ws = std::max(ws, (size_t)dense_fwd_split3_splits(l.out_units, l.in_units, net->num_sms) * B * l.out_units * 4);
       long long bps = simt_tiles((int)B, l.out_units);
       int sp = simt_splits(l.in_units, pick_splits(bps, l.in_units, 256, net->num_sms, 8, 256));
       ws = std::max(ws, (size_t)sp * B * l.out_units * 4);

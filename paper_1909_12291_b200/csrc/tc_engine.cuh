@@ -95,6 +95,17 @@ struct EpiWarpsSync<Epi, std::void_t<decltype(Epi::EPI_WARPS_SYNC)>> {
   static constexpr int value = Epi::EPI_WARPS_SYNC;
 };
 
+// Loader::SPLIT3: fp32-accurate GEMM on the bf16 tensor cores (fp32 check mode).
+// The producers store every fp32 operand value as three bf16 planes
+// (v = hi + mid + lo, each the bf16 rounding of the remainder), and every K=16
+// step issues the six products with a combined weight >= 2^-16:
+//   lo*hi + mid*mid + hi*lo + mid*hi + hi*mid + hi*hi   (smallest first)
+// accumulated in fp32 in TMEM; the dropped terms are below 2^-24 relative.
+template <class Loader, class = void>
+struct Split3 : std::false_type {};
+template <class Loader>
+struct Split3<Loader, std::void_t<decltype(Loader::SPLIT3)>> : std::bool_constant<Loader::SPLIT3> {};
+
 template <class Loader, class Epi>
 struct TcRoles {
   static constexpr int PW = ProducerWarps<Loader>::value;
@@ -159,16 +170,21 @@ __device__ inline TileCoord tc_tile(const TcShape& s, int t, int bn) {
   return c;
 }
 
-template <int BN, int EPI_STAGE = 0>
+template <int BN, int EPI_STAGE = 0, int PLANES = 1>
 struct TcSmemLayout {
-  static constexpr int A_BYTES = TC_BM * TC_BK * 2;  // 16 KB
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int A_PLANE = TC_BM * TC_BK * 2;  // 16 KB
+  static constexpr int B_PLANE = BN * TC_BK * 2;
+  static constexpr int A_BYTES = A_PLANE * PLANES;
+  static constexpr int B_BYTES = B_PLANE * PLANES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // pipeline budget: 196 KB less any epilogue staging beyond the 8 KB of 8 staged warps
   static constexpr int RING = 196 * 1024 - (EPI_STAGE > 8192 ? EPI_STAGE - 8192 : 0);
   static constexpr int STAGES = (RING / STAGE_BYTES) > 8 ? 8 : (RING / STAGE_BYTES);
   static constexpr int LAG = STAGES - 1 > TC_MAX_LAG ? TC_MAX_LAG : STAGES - 1;  // cp.async groups in flight
-  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  // SPLIT3 keeps two accumulators per buffer (hi*hi and the cross terms)
+  static constexpr int ACC_COLS = (PLANES == 3 ? 2 : 1) * BN;
+  static constexpr int TMEM_COLS = (2 * ACC_COLS <= 32) ? 32 : (2 * ACC_COLS <= 64) ? 64 : (2 * ACC_COLS <= 128) ? 128
+                                   : (2 * ACC_COLS <= 256) ? 256 : 512;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
   static constexpr int TOTAL = STAGES * STAGE_BYTES + TC_TABLE_BYTES + BAR_BYTES + EPI_STAGE + 1024;  // + slack
 };
@@ -179,7 +195,8 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
   using R = TcRoles<Loader, Epi>;
   constexpr bool STAGED = EpiStaged<Epi>::value;
   constexpr int WSM = EpiWarpSmem<Epi>::value;
-  using L = TcSmemLayout<BN, R::EPI_STAGE>;
+  constexpr bool SPLIT = Split3<Loader>::value;
+  using L = TcSmemLayout<BN, R::EPI_STAGE, SPLIT ? 3 : 1>;
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -274,7 +291,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * L::ACC_COLS);
       if constexpr (STAGED) {
         // software-pipelined: the TMEM load of the next chunk is in flight while this
         // one is converted, staged (XOR-swizzled halves: conflict-free both ways) and
@@ -318,10 +335,18 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
         for (int col = col_begin; col < col_end; col += 16) {
           uint32_t r[16];
           tmem_ld16(tbase + col, r);
-          tmem_ld_wait();
           float v[16];
+          if constexpr (SPLIT) {  // hi*hi + cross terms, added in IEEE fp32
+            uint32_t r2[16];
+            tmem_ld16(tbase + BN + col, r2);
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+            for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) + __uint_as_float(r2[i]);
+          } else {
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+          }
           if constexpr (WSM > 0)
             epi.store_warp(c, q, col, v, epi_stage + (warp - R::PW) * WSM);
           else
@@ -344,7 +369,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
       const int acc = lt & 1;
       mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * L::ACC_COLS);
       for (int kb = 0; kb < c.nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -356,6 +381,23 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
           if (nk16 > TC_BK / 16) nk16 = TC_BK / 16;
 #pragma unroll 1
           for (int k = 0; k < nk16; ++k) {
+            if constexpr (SPLIT) {
+              // six plane products (no-swizzle canonical layouts): the five cross terms,
+              // smallest first, into a second accumulator so the hi*hi chain (the large
+              // one) takes a single accumulation per K=16 step; the epilogue adds the two
+              constexpr int PA[6] = {2, 1, 0, 1, 0, 0}, PB[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll
+              for (int q = 0; q < 6; ++q) {
+                const uint64_t ad =
+                    make_sdesc(sA + (uint32_t)PA[q] * L::A_PLANE + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
+                const uint64_t bd =
+                    make_sdesc(sB + (uint32_t)PB[q] * L::B_PLANE + (uint32_t)(2 * k) * (BN * 16), BN * 16, 128);
+                const bool big = q == 5;
+                umma_bf16(d_tmem + (big ? 0u : (uint32_t)BN), ad, bd, idesc,
+                          (kb > 0 || k > 0 || (!big && q > 0)) ? 1u : 0u);
+              }
+              continue;
+            }
             // K-major: a K=16 step covers chunks 2k, 2k+1 (LBO apart).
             // MN-major: a K=16 step covers K groups 2k, 2k+1 (LBO apart).
             uint64_t ad;
@@ -402,7 +444,7 @@ __device__ __forceinline__ uint32_t mnmajor_off(int R, int g, int kk) {
 
 template <int BN, class Loader, class Epi>
 inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& shape, int num_sms, cudaStream_t st) {
-  using L = TcSmemLayout<BN, TcRoles<Loader, Epi>::EPI_STAGE>;
+  using L = TcSmemLayout<BN, TcRoles<Loader, Epi>::EPI_STAGE, Split3<Loader>::value ? 3 : 1>;
   auto kern = tc_gemm_kernel<BN, Loader, Epi>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
   if (e != cudaSuccess) return e;
