@@ -726,15 +726,84 @@ inline int with_bn(int n, Fn&& fn) {
   return fn(std::integral_constant<int, 256>());
 }
 
+// Split-K partials of a sub-wave conv forward: part[split][m][o] (fp32, o contiguous)
+struct FwdPartialEpi {
+  float* part;
+  int M, co;
+  __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
+    const int m = c.m0 + row, o0 = c.n0 + col;
+    if (m >= M || o0 >= co) return;
+    float4* p = (float4*)(part + ((size_t)c.split * M + m) * co + o0);
+    p[0] = make_float4(v[0], v[1], v[2], v[3]);
+    p[1] = make_float4(v[4], v[5], v[6], v[7]);
+    if (o0 + 8 < co) {
+      p[2] = make_float4(v[8], v[9], v[10], v[11]);
+      p[3] = make_float4(v[12], v[13], v[14], v[15]);
+    }
+  }
+  __device__ void finish(int, int) const {}
+};
+
+// y[m][o] = ReLU?(sum over splits in order + bias) as bf16, 8 channels per thread
+__global__ void __launch_bounds__(256) conv_fwd_reduce_kernel(const float* __restrict__ part, int splits, int M,
+                                                              int co, const float* __restrict__ bias, int relu,
+                                                              bf16* __restrict__ y) {
+  const int cg = co / 8;
+  const size_t total = (size_t)M * cg, plane = (size_t)M * co;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int o0 = (int)(e % cg) * 8;
+    const size_t off = (e / cg) * co + o0;
+    float acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float4 a = __ldcs((const float4*)(part + s * plane + off)), b = __ldcs((const float4*)(part + s * plane + off) + 1);
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+      acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+    }
+    __align__(16) bf16 out[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      float t = acc[u] + bias[o0 + u];
+      if (relu) t = t > 0.f ? t : 0.f;
+      out[u] = __float2bfloat16_rn(t);
+    }
+    *(uint4*)(y + off) = *(const uint4*)out;
+  }
+}
+
+// Split count of a conv forward: 1 when its tiles fill at least half the GPU; else enough
+// splits for about one wave, each keeping >= 8 K blocks (the partials cost 4 B per output
+// per split, so long-K, small-M layers gain the most: late layers on small maps)
+inline int conv_fwd_splits(const ConvGeom& g, int num_sms) {
+  static const int off = [] {
+    const char* e = getenv("CE_CONV_FWD_SPLITK");
+    return e && e[0] == '0';
+  }();
+  const int M = g.n * g.oh * g.ow, K = g.k * g.k * g.c;
+  const int m_tiles = (M + TC_BM - 1) / TC_BM, nkb = (K + TC_BK - 1) / TC_BK;
+  const int tiles = m_tiles * ((g.co + 255) / 256);
+  if (off || 2 * tiles >= num_sms || nkb < 16) return 1;
+  int s = num_sms / tiles;
+  s = std::min(s, nkb / 8);
+  s = std::min(s, 16);
+  return s < 2 ? 1 : s;
+}
+inline size_t conv_fwd_ws_bytes(const ConvGeom& g, int num_sms) {
+  const int s = conv_fwd_splits(g, num_sms);
+  return s > 1 ? (size_t)s * g.n * g.oh * g.ow * g.co * 4 : 0;
+}
+
+// ws / ws_bytes: split-K partials for sub-wave layers (nullptr: never split)
 inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const float* bias, int relu, bf16* y,
-                       int num_sms, cudaStream_t st) {
+                       int num_sms, cudaStream_t st, float* ws = nullptr, size_t ws_bytes = 0) {
   const int M = g.n * g.oh * g.ow, K = g.k * g.k * g.c;
   if ((K / 8) * 4 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_fwd_tc: K=%d exceeds the chunk table", K);
-  return with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.co, num_sms), [&](auto bn) {
+  int splits = ws ? conv_fwd_splits(g, num_sms) : 1;
+  if (splits > 1 && (size_t)splits * M * g.co * 4 > ws_bytes) splits = 1;
+  auto launch = [&](auto bn, const auto& ep, int nsplit) {
     constexpr int BN = decltype(bn)::value;
-    TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
-    FwdTcEpi ep{y, bias, M, g.co, relu};
-    cudaError_t e;
+    TcShape sh = tc_make_shape(M, g.co, K, BN, nsplit);
     const bool tma = !tma_disabled();
     auto fill = [&](auto& ld) {
       ld.x = x; ld.w = w; ld.g = g; ld.K = K; ld.M = M; ld.BN = BN;
@@ -746,19 +815,32 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
     if (tma && g.c % 64 == 0 && !im2col_disabled() && make_tmap_kmajor(&ld2.wmap, w, g.co, K, BN) &&
         make_tmap_im2col(&ld2.xmap, x, g, TC_BM)) {
       fill(ld2);
-      e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
-    } else if (tma && narrow_im2col_enabled() && make_tmap_kmajor(&ld3.wmap, w, g.co, K, BN) &&
-               make_tmap_im2col(&ld3.xmap, x, g, TC_BM, 8)) {
-      fill(ld3);
-      e = tc_launch<BN>(ld3, ep, sh, num_sms, st);
-    } else if (tma && make_tmap_kmajor(&ld1.wmap, w, g.co, K, BN)) {
-      fill(ld1);
-      e = tc_launch<BN>(ld1, ep, sh, num_sms, st);
-    } else {
-      FwdTcLoader<0> ld{};
-      fill(ld);
-      e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+      return tc_launch<BN>(ld2, ep, sh, num_sms, st);
     }
+    if (tma && narrow_im2col_enabled() && make_tmap_kmajor(&ld3.wmap, w, g.co, K, BN) &&
+        make_tmap_im2col(&ld3.xmap, x, g, TC_BM, 8)) {
+      fill(ld3);
+      return tc_launch<BN>(ld3, ep, sh, num_sms, st);
+    }
+    if (tma && make_tmap_kmajor(&ld1.wmap, w, g.co, K, BN)) {
+      fill(ld1);
+      return tc_launch<BN>(ld1, ep, sh, num_sms, st);
+    }
+    FwdTcLoader<0> ld{};
+    fill(ld);
+    return tc_launch<BN>(ld, ep, sh, num_sms, st);
+  };
+  if (splits > 1) {  // sub-wave layer: split-K partials, then bias + ReLU + bf16 in one pass
+    return with_bn(g.co, [&](auto bn) {
+      cudaError_t e = launch(bn, FwdPartialEpi{ws, M, g.co}, splits);
+      if (e != cudaSuccess) return fail(CE_ECUDA, "conv_fwd_tc split-K: %s", cudaGetErrorString(e));
+      conv_fwd_reduce_kernel<<<grid_for((size_t)M * (g.co / 8)), 256, 0, st>>>(ws, splits, M, g.co, bias, relu, y);
+      e = cudaGetLastError();
+      return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_reduce: %s", cudaGetErrorString(e));
+    });
+  }
+  return with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.co, num_sms), [&](auto bn) {
+    cudaError_t e = launch(bn, FwdTcEpi{y, bias, M, g.co, relu}, 1);
     return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc: %s", cudaGetErrorString(e));
   });
 }

@@ -302,6 +302,95 @@ __global__ void __launch_bounds__(256) head_bwd_kernel(const TX* __restrict__ x,
   }
 }
 
+// Narrow inputs (in <= kHeadBwdSmallIn): the one-thread-per-4-columns kernel above has
+// a single CTA whose threads walk all B rows serially (latency-bound, ~37 us for the
+// FIXED 64 -> 2 head at B = 64). Here a CTA owns 64 columns and its 16 row groups
+// split the batch: thread (cq, rg) takes columns 4cq..4cq+3 of rows rg, rg+16, ...;
+// dX of those (row, column) pairs is complete in-thread, the dW partials of the 16
+// row groups are added in a fixed order in shared memory (deterministic), then the
+// momentum update runs as in head_bwd_kernel.
+constexpr int kHeadBwdSmallIn = 4096;
+template <class TX, class TD, int OUT>
+__global__ void __launch_bounds__(256) head_bwd_small_kernel(const TX* __restrict__ x, int x_ld,
+                                                             const float* __restrict__ g, int B, int in,
+                                                             float* __restrict__ w, float* __restrict__ vel,
+                                                             float* __restrict__ gw, TD* __restrict__ dx,
+                                                             const TD* __restrict__ mask, float* __restrict__ b,
+                                                             float* __restrict__ vb, float* __restrict__ gb, float lr,
+                                                             float mu) {
+  __shared__ float Gs[kHeadMaxBatch][OUT];
+  __shared__ float red[16][OUT][64];
+  for (int e = threadIdx.x; e < B * OUT; e += blockDim.x) Gs[e / OUT][e % OUT] = g[e];
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < OUT) {  // bias: sum over the batch in order
+    const int o = threadIdx.x;
+    float s = 0.f;
+    for (int r = 0; r < B; ++r) s += Gs[r][o];
+    if (gb) gb[o] = s;
+    float bv = b[o], v = vb[o];
+    sgd_update(bv, v, s, lr, mu);
+    b[o] = bv;
+    vb[o] = v;
+  }
+  const int cq = threadIdx.x & 15, rg = threadIdx.x >> 4;
+  const int i0 = blockIdx.x * 64 + cq * 4;
+  const int nj = i0 < in ? min(4, in - i0) : 0;
+  float wv[OUT][4], acc[OUT][4];
+#pragma unroll
+  for (int o = 0; o < OUT; ++o)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      wv[o][j] = j < nj ? w[(size_t)o * in + i0 + j] : 0.f;
+      acc[o][j] = 0.f;
+    }
+  for (int r = rg; r < B; r += 16) {
+    float xv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xv[j] = j < nj ? ldf(x, (size_t)r * x_ld + i0 + j) : 0.f;
+    float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int o = 0; o < OUT; ++o) {
+      const float gr = Gs[r][o];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[o][j] = fmaf(gr, xv[j], acc[o][j]);
+        d[j] = fmaf(gr, wv[o][j], d[j]);
+      }
+    }
+    if (dx) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= nj) break;
+        const size_t off = (size_t)r * in + i0 + j;
+        float v = d[j];
+        if (mask && !(ldf(mask, off) > 0.f)) v = 0.f;
+        stf(dx, off, v);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < OUT; ++o)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[rg][o][cq * 4 + j] = acc[o][j];
+  __syncthreads();
+  if (rg != 0 || nj == 0) return;
+#pragma unroll
+  for (int o = 0; o < OUT; ++o) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= nj) break;
+      float s = 0.f;
+      for (int q = 0; q < 16; ++q) s += red[q][o][cq * 4 + j];  // row groups in order
+      const size_t off = (size_t)o * in + i0 + j;
+      if (gw) gw[off] = s;
+      float wq = wv[o][j], vq = vel[off];
+      sgd_update(wq, vq, s, lr, mu);
+      w[off] = wq;
+      vel[off] = vq;
+    }
+  }
+}
+
 // column chunks of the forward; rows are split over cdiv(B, kHeadRowsPerCta) CTAs
 inline int head_fwd_grid(int in, int num_sms, int B = kHeadRowsPerCta) {
   const int rows = (B + kHeadRowsPerCta - 1) / kHeadRowsPerCta;
@@ -337,10 +426,15 @@ inline int launch_head_bwd(const TX* x, int x_ld, const float* g, int B, int in,
                            float* gw, TD* dx, const TD* mask, float* b, float* vb, float* gb, float lr, float mu,
                            cudaStream_t st) {
   const int grid = (in + 1023) / 1024;
-#define CE_HEAD_B(O)                                                                                              \
-  if (out == O) {                                                                                                 \
-    head_bwd_kernel<TX, TD, O><<<grid, 256, 0, st>>>(x, x_ld, g, B, in, w, vel, gw, dx, mask, b, vb, gb, lr, mu); \
-    return CE_OK;                                                                                                 \
+  const bool small = in <= kHeadBwdSmallIn;
+#define CE_HEAD_B(O)                                                                                                \
+  if (out == O) {                                                                                                   \
+    if (small)                                                                                                      \
+      head_bwd_small_kernel<TX, TD, O><<<(in + 63) / 64, 256, 0, st>>>(x, x_ld, g, B, in, w, vel, gw, dx, mask, b, \
+                                                                       vb, gb, lr, mu);                             \
+    else                                                                                                            \
+      head_bwd_kernel<TX, TD, O><<<grid, 256, 0, st>>>(x, x_ld, g, B, in, w, vel, gw, dx, mask, b, vb, gb, lr, mu); \
+    return CE_OK;                                                                                                   \
   }
   CE_HEAD_B(1) CE_HEAD_B(2) CE_HEAD_B(3) CE_HEAD_B(4)
 #undef CE_HEAD_B

@@ -425,7 +425,8 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
           conv_fwd_packed_simt(g, (const float*)l.xcol, l.Kp, l.Wpf, l.b, l.relu, (float*)l.out, st);
         }
       } else if (net->use_tc) {
-        int s = conv_fwd_tc(g, (const bf16*)in, l.Wbf, l.b, l.relu, (bf16*)l.out, net->num_sms, st);
+        int s = conv_fwd_tc(g, (const bf16*)in, l.Wbf, l.b, l.relu, (bf16*)l.out, net->num_sms, st, net->ws,
+                            net->ws_bytes);
         if (s != CE_OK) return s;
       } else {
         simt_gemm(make_fwd_a((const T*)in, g), FwdB{l.W, K}, FwdEpi<T>{(T*)l.out, l.b, g.co, l.relu != 0}, M, g.co, K,
@@ -1064,6 +1065,10 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         int sp = simt_splits((int)Mo, pick_splits(bps, Mo, 512, net->num_sms));
         sp = std::max(sp, conv_wgrad_tc_max_splits(l.g, (int)B, net->num_sms));
         ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);
+        if (net->use_tc) {  // split-K partials of a sub-wave forward, for any batch the net may run
+          ConvGeom gb = l.g;
+          for (gb.n = 1; gb.n <= (int)B; ++gb.n) ws = std::max(ws, conv_fwd_ws_bytes(gb, net->num_sms));
+        }
         l.col2im = net->use_tc && l.need_dx && col2im_dgrad_eligible(l.g);
         if (l.col2im) zbytes = std::max(zbytes, col2im_dgrad_zbytes(l.g, (int)B));
         if (l.packed) {
