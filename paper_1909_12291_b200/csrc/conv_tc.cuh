@@ -847,13 +847,111 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
 
 // Conv forward + non-overlapping max-pool in one kernel (window-major rows,
 // FwdPoolEpi): y / arg are the POOLED map [n][PH][PW][co] and its argmax.
+// Sub-wave conv + pool: the split-K partials of the window-major rows are summed in
+// split order, biased, ReLU'd and rounded to bf16 exactly as FwdPoolEpi does, then
+// pooled with its first-max rule (one thread per window x 8 channels).
+template <int KK>
+__global__ void __launch_bounds__(256) conv_pool_reduce_kernel(const float* __restrict__ part, int splits, int rows,
+                                                               int co, const float* __restrict__ bias, int relu,
+                                                               PoolMap pm, bf16* __restrict__ y,
+                                                               uint8_t* __restrict__ arg) {
+  const int cg = co / 8;
+  const size_t total = (size_t)pm.windows * cg, plane = (size_t)rows * co;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int o0 = (int)(e % cg) * 8;
+    const int window = (int)(e / cg);
+    const int t = window / pm.WPT, r = window - t * pm.WPT, wq = r / pm.WPW, wl = r - wq * pm.WPW;
+    const int row0 = t * TC_BM + wq * 32 + wl * KK;
+    float best[8];
+    uint8_t bi[8];
+#pragma unroll 1
+    for (int tap = 0; tap < KK; ++tap) {
+      const size_t off = (size_t)(row0 + tap) * co + o0;
+      float acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+      for (int s = 0; s < splits; ++s) {
+        const float4 a = __ldcs((const float4*)(part + s * plane + off));
+        const float4 b = __ldcs((const float4*)(part + s * plane + off) + 1);
+        acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+        acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float v = acc[u] + bias[o0 + u];
+        if (relu) v = v > 0.f ? v : 0.f;
+        v = __bfloat162float(__float2bfloat16_rn(v));
+        if (tap == 0 || v > best[u]) {
+          best[u] = v;
+          bi[u] = (uint8_t)tap;
+        }
+      }
+    }
+    __align__(16) bf16 out[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      out[u] = __float2bfloat16_rn(best[u]);
+      if (relu && !(best[u] > 0.f)) bi[u] = kPoolDead;
+    }
+    const size_t dst = (size_t)window * co + o0;
+    *(uint4*)(y + dst) = *(const uint4*)out;
+    *(uint2*)(arg + dst) = *(const uint2*)bi;
+  }
+}
+
+inline int conv_pool_splits(const ConvGeom& g, const PoolMap& pm, int num_sms) {
+  ConvGeom q = g;  // the split rule of conv_fwd_splits on the window-major row count
+  const int rows = pool_rows(pm);
+  q.n = 1;
+  q.oh = rows;
+  q.ow = 1;
+  return conv_fwd_splits(q, num_sms);
+}
+inline size_t conv_pool_ws_bytes(const ConvGeom& g, int ps, int pst, int num_sms) {
+  const PoolMap pm = make_pool_map(g.n, g.oh, g.ow, ps, pst);
+  const int s = conv_pool_splits(g, pm, num_sms);
+  return s > 1 ? (size_t)s * pool_rows(pm) * g.co * 4 : 0;
+}
+
 inline int conv_fwd_tc_pool(const ConvGeom& g, const bf16* x, const bf16* w, const float* bias, int relu, int ps,
-                            int pst, bf16* y, uint8_t* arg, int num_sms, cudaStream_t st) {
+                            int pst, bf16* y, uint8_t* arg, int num_sms, cudaStream_t st, float* ws = nullptr,
+                            size_t ws_bytes = 0) {
   if (!pool_fusable(ps, pst)) return fail(CE_EINVAL, "pool epilogue needs a non-overlapping 2x2 or 3x3 window");
   const int K = g.k * g.k * g.c;
   if ((K / 8) * 4 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_fwd_tc_pool: K=%d exceeds the chunk table", K);
   const PoolMap pm = make_pool_map(g.n, g.oh, g.ow, ps, pst);
   const int Mp = pool_rows(pm);
+  int splits = ws ? conv_pool_splits(g, pm, num_sms) : 1;
+  if (splits > 1 && (size_t)splits * Mp * g.co * 4 > ws_bytes) splits = 1;
+  if (splits > 1) {  // sub-wave: split-K partials over the window-major rows, then pool in the reduce
+    return with_bn(g.co, [&](auto bn) {
+      constexpr int BN = decltype(bn)::value;
+      TcShape sh = tc_make_shape(Mp, g.co, K, BN, splits);
+      FwdPartialEpi ep{ws, Mp, g.co};
+      auto fill = [&](auto& ld) {
+        ld.x = x; ld.w = w; ld.g = g; ld.K = K; ld.M = Mp; ld.BN = BN; ld.pm = pm;
+        ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      };
+      cudaError_t e;
+      FwdTcLoader<1, true> ld1{};
+      if (!tma_disabled() && make_tmap_kmajor(&ld1.wmap, w, g.co, K, BN)) {
+        fill(ld1);
+        e = tc_launch<BN>(ld1, ep, sh, num_sms, st);
+      } else {
+        FwdTcLoader<0, true> ld0{};
+        fill(ld0);
+        e = tc_launch<BN>(ld0, ep, sh, num_sms, st);
+      }
+      if (e != cudaSuccess) return fail(CE_ECUDA, "conv_fwd_tc_pool split-K: %s", cudaGetErrorString(e));
+      const unsigned grid = grid_for((size_t)pm.windows * (g.co / 8));
+      if (ps == 2)
+        conv_pool_reduce_kernel<4><<<grid, 256, 0, st>>>(ws, splits, Mp, g.co, bias, relu, pm, y, arg);
+      else
+        conv_pool_reduce_kernel<9><<<grid, 256, 0, st>>>(ws, splits, Mp, g.co, bias, relu, pm, y, arg);
+      e = cudaGetLastError();
+      return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_pool_reduce: %s", cudaGetErrorString(e));
+    });
+  }
   return with_bn(pick_bn(Mp / TC_BM, g.co, num_sms), [&](auto bn) {
     constexpr int BN = decltype(bn)::value;
     return with_pool_kk(ps, [&](auto kkc) {

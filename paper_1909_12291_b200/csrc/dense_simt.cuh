@@ -538,6 +538,216 @@ inline int dense_fwd_simt(const TX* x, const float* w, int B, int in, int out, i
   }
 }
 
+// ------------------------------------------------------------------ streaming-W FFMA (fp32 check mode)
+// Wide fp32 layers at small batch (C2 #15: 262144 -> 523 at B = 32) are bound by the
+// FMA pipe, not HBM: 2 FMAs per weight per row. These kernels give every weight to
+// exactly one thread, straight from HBM into registers (prefetched one chunk ahead),
+// and keep the small operand (x or the output gradient) in shared memory, read as
+// warp-uniform float4 broadcasts: 8 FMAs per shared-memory load.
+constexpr int DW_KC = 16;     // k per chunk
+constexpr int DW_THREADS = 64;
+
+// part[split][b][o] = sum over the split's k-range of x[b][k] w[o][k]; thread -> outputs
+// o = base + tid + 64 j (j < 2), all BR rows of a row block
+template <int BR>
+__global__ void __launch_bounds__(DW_THREADS) dense_fwd_stream_kernel(const float* __restrict__ x,
+                                                                      const float* __restrict__ w, int B, int in,
+                                                                      int out, int kchunk, float* __restrict__ part) {
+  constexpr int R = 2, XS = DW_KC + 4;
+  __shared__ __align__(16) float xs[2][BR][XS];
+  const int tid = threadIdx.x;
+  const int ob = blockIdx.x * (DW_THREADS * R), bb = blockIdx.y * BR;
+  const int k0 = blockIdx.z * kchunk, k1 = min(in, k0 + kchunk);
+  float4 wc[R][DW_KC / 4], wn[R][DW_KC / 4];
+  float acc[R][BR];
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int b = 0; b < BR; ++b) acc[j][b] = 0.f;
+  auto fetch_w = [&](int kc, float4 (&dst)[R][DW_KC / 4]) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int o = ob + tid + DW_THREADS * j;
+#pragma unroll
+      for (int q = 0; q < DW_KC / 4; ++q) {
+        const int k = kc + 4 * q;
+        dst[j][q] = (o < out && k < k1) ? __ldcs((const float4*)(w + (size_t)o * in + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  auto fetch_x = [&](int kc, int buf) {  // BR rows x 16 k: 4*BR float4, DW_THREADS threads
+    for (int e = tid; e < BR * (DW_KC / 4); e += DW_THREADS) {
+      const int r = e / (DW_KC / 4), q = e % (DW_KC / 4), k = kc + 4 * q, b = bb + r;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (b < B && k < k1) v = *(const float4*)(x + (size_t)b * in + k);
+      *(float4*)&xs[buf][r][4 * q] = v;
+    }
+  };
+  int buf = 0;
+  if (k0 < k1) {
+    fetch_w(k0, wc);
+    fetch_x(k0, 0);
+  }
+  __syncthreads();
+  for (int kc = k0; kc < k1; kc += DW_KC) {
+    const bool more = kc + DW_KC < k1;
+    if (more) fetch_w(kc + DW_KC, wn);
+#pragma unroll
+    for (int q = 0; q < DW_KC / 4; ++q) {
+#pragma unroll
+      for (int b = 0; b < BR; ++b) {
+        const float4 xv = *(const float4*)&xs[buf][b][4 * q];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          float a = acc[j][b];
+          a = fmaf(xv.x, wc[j][q].x, a);
+          a = fmaf(xv.y, wc[j][q].y, a);
+          a = fmaf(xv.z, wc[j][q].z, a);
+          a = fmaf(xv.w, wc[j][q].w, a);
+          acc[j][b] = a;
+        }
+      }
+    }
+    if (more) fetch_x(kc + DW_KC, buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+#pragma unroll
+      for (int q = 0; q < DW_KC / 4; ++q) wc[j][q] = wn[j][q];
+  }
+  float* dst = part + (size_t)blockIdx.z * B * out;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int o = ob + tid + DW_THREADS * j;
+    if (o >= out) continue;
+#pragma unroll
+    for (int b = 0; b < BR; ++b)
+      if (bb + b < B) dst[(size_t)(bb + b) * out + o] = acc[j][b];
+  }
+}
+
+// dx[b][i] = sum_o g[b][o] w[o][i] (pre-update weights), gated by (mask > 0): thread -> inputs
+// i, i+1 (float2 of every weight row, coalesced across the warp), all BR rows
+template <int BR, class TM>
+__global__ void __launch_bounds__(DW_THREADS) dense_dx_stream_kernel(const float* __restrict__ g,
+                                                                     const float* __restrict__ w, int B, int in,
+                                                                     int out, const TM* __restrict__ mask,
+                                                                     float* __restrict__ dx) {
+  constexpr int GS = DW_KC + 4;
+  __shared__ __align__(16) float gs[2][BR][GS];
+  const int tid = threadIdx.x;
+  const int i = blockIdx.x * (2 * DW_THREADS) + 2 * tid, bb = blockIdx.y * BR;
+  const bool ok = i + 1 < in;  // in % 2 == 0 (caller)
+  float2 wc[DW_KC], wn[DW_KC];
+  float acc[2][BR];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int b = 0; b < BR; ++b) acc[u][b] = 0.f;
+  auto fetch_w = [&](int oc, float2 (&dst)[DW_KC]) {
+#pragma unroll
+    for (int q = 0; q < DW_KC; ++q) {
+      const int o = oc + q;
+      dst[q] = (ok && o < out) ? __ldcs((const float2*)(w + (size_t)o * in + i)) : make_float2(0.f, 0.f);
+    }
+  };
+  auto fetch_g = [&](int oc, int buf) {
+    for (int e = tid; e < BR * DW_KC; e += DW_THREADS) {
+      const int r = e / DW_KC, q = e % DW_KC, o = oc + q, b = bb + r;
+      gs[buf][r][q] = (b < B && o < out) ? g[(size_t)b * out + o] : 0.f;
+    }
+  };
+  int buf = 0;
+  fetch_w(0, wc);
+  fetch_g(0, 0);
+  __syncthreads();
+  for (int oc = 0; oc < out; oc += DW_KC) {
+    const bool more = oc + DW_KC < out;
+    if (more) fetch_w(oc + DW_KC, wn);
+#pragma unroll
+    for (int q = 0; q < DW_KC / 4; ++q) {
+#pragma unroll
+      for (int b = 0; b < BR; ++b) {
+        const float4 gv = *(const float4*)&gs[buf][b][4 * q];
+        float a0 = acc[0][b], a1 = acc[1][b];
+        a0 = fmaf(gv.x, wc[4 * q].x, a0);
+        a1 = fmaf(gv.x, wc[4 * q].y, a1);
+        a0 = fmaf(gv.y, wc[4 * q + 1].x, a0);
+        a1 = fmaf(gv.y, wc[4 * q + 1].y, a1);
+        a0 = fmaf(gv.z, wc[4 * q + 2].x, a0);
+        a1 = fmaf(gv.z, wc[4 * q + 2].y, a1);
+        a0 = fmaf(gv.w, wc[4 * q + 3].x, a0);
+        a1 = fmaf(gv.w, wc[4 * q + 3].y, a1);
+        acc[0][b] = a0;
+        acc[1][b] = a1;
+      }
+    }
+    if (more) fetch_g(oc + DW_KC, buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+#pragma unroll
+    for (int q = 0; q < DW_KC; ++q) wc[q] = wn[q];
+  }
+  if (!ok) return;
+#pragma unroll
+  for (int b = 0; b < BR; ++b) {
+    if (bb + b >= B) break;
+    const size_t off = (size_t)(bb + b) * in + i;
+    float v0 = acc[0][b], v1 = acc[1][b];
+    if (mask) {
+      if (!(ldf(mask, off) > 0.f)) v0 = 0.f;
+      if (!(ldf(mask, off + 1) > 0.f)) v1 = 0.f;
+    }
+    *(float2*)(dx + off) = make_float2(v0, v1);
+  }
+}
+
+// fp32 layers that take the streaming kernels: wide (>= 1 M weights), B <= 64, rows of
+// 16 B (in % 4 == 0). Opt-in (CE_DENSE_STREAM=1): on C2 #15 (262144 -> 523, B = 32) they
+// measured slower than the tiled kernels (forward 413 vs 335 us, backward 812 vs 703 us):
+// the per-lane weight rows scatter every warp load over 32 DRAM rows.
+inline bool dense_stream_enabled(int B, int in, long long params) {
+  static const bool on = [] {
+    const char* e = getenv("CE_DENSE_STREAM");
+    return e && e[0] == '1';
+  }();
+  return on && B <= 64 && (in & 3) == 0 && params >= (1ll << 20);
+}
+inline int dense_fwd_stream_splits(int B, int in, int out, int num_sms) {
+  const long long blocks = (long long)((out + 2 * DW_THREADS - 1) / (2 * DW_THREADS)) * ((B + 31) / 32);
+  long long s = (6LL * num_sms + blocks - 1) / blocks;  // ~6 resident 64-thread CTAs per SM
+  const long long cap = (in + 255) / 256;
+  if (s > cap) s = cap;
+  if (s > 512) s = 512;
+  return s < 1 ? 1 : (int)s;
+}
+// returns the split count written to part
+inline int dense_fwd_stream(const float* x, const float* w, int B, int in, int out, int splits, float* part,
+                            cudaStream_t st) {
+  const int kchunk = ((in + splits - 1) / splits + DW_KC - 1) / DW_KC * DW_KC;
+  const int s = (in + kchunk - 1) / kchunk;
+  if (B <= 16) {
+    dim3 grid((out + 2 * DW_THREADS - 1) / (2 * DW_THREADS), (B + 15) / 16, s);
+    dense_fwd_stream_kernel<16><<<grid, DW_THREADS, 0, st>>>(x, w, B, in, out, kchunk, part);
+  } else {
+    dim3 grid((out + 2 * DW_THREADS - 1) / (2 * DW_THREADS), (B + 31) / 32, s);
+    dense_fwd_stream_kernel<32><<<grid, DW_THREADS, 0, st>>>(x, w, B, in, out, kchunk, part);
+  }
+  return s;
+}
+template <class TM>
+inline void dense_dx_stream(const float* g, const float* w, int B, int in, int out, const TM* mask, float* dx,
+                            cudaStream_t st) {
+  if (B <= 16) {
+    dim3 grid((in + 2 * DW_THREADS - 1) / (2 * DW_THREADS), (B + 15) / 16);
+    dense_dx_stream_kernel<16, TM><<<grid, DW_THREADS, 0, st>>>(g, w, B, in, out, mask, dx);
+  } else {
+    dim3 grid((in + 2 * DW_THREADS - 1) / (2 * DW_THREADS), (B + 31) / 32);
+    dense_dx_stream_kernel<32, TM><<<grid, DW_THREADS, 0, st>>>(g, w, B, in, out, mask, dx);
+  }
+}
+
 // fp32 check mode: these kernels up to B = 64, the generic SIMT GEMM above.
 constexpr int kDenseSimtMaxBatch = 64;
 // bf16: measured on B200 (C2 heads, 51-137 M params): the FFMA dW+SGD pass

@@ -344,12 +344,14 @@ void prof_collect(ce_net* net, bool keep = false) {
 }
 
 // CE_POOL_FUSION: 0 = never fuse max-pool into the conv epilogue, 1 = only where
-// the conv runs the gather loader anyway (packed first layer, C % 64 != 0),
-// 2 = every non-overlapping pool after a conv (default)
+// the conv runs the gather loader anyway (packed first layer, C % 64 != 0; default),
+// 2 = every non-overlapping pool after a conv. The window-major row order needs the
+// gather loader, which is slower than the TMA im2col loader on C % 64 == 0 layers:
+// with mode 2 VGG16STYLE inference (three such pools) fell from 126k to 79k patches/s.
 int pool_fusion_mode() {
   static const int mode = [] {
     const char* e = getenv("CE_POOL_FUSION");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
   }();
   return mode;
 }
@@ -398,7 +400,7 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
         if (s != CE_OK) return s;
       } else {
         int s = conv_fwd_tc_pool(g, (const bf16*)in, l.Wbf, l.b, l.relu, pl.g.k, pl.g.s, (bf16*)pl.out, pl.arg,
-                                 net->num_sms, st);
+                                 net->num_sms, st, net->ws, net->ws_bytes);
         if (s != CE_OK) return s;
       }
       CE_CHECK_LAUNCH();
@@ -477,6 +479,10 @@ int enqueue_forward(ce_net* net, int n, bool loss = false, bool* loss_fused = nu
       } else if (dense_split3_enabled(B, (long long)K * O)) {  // fp32 check mode on the tensor cores
         int s = dense_fwd_split3((const float*)in, K, l.W, K, O, B, net->ws, &splits, net->num_sms, st);
         if (s != CE_OK) return s;
+      } else if (dense_stream_enabled(B, K, (long long)K * O) &&
+                 (size_t)dense_fwd_stream_splits(B, K, O, net->num_sms) * B * O * 4 <= net->ws_bytes) {
+        splits = dense_fwd_stream((const float*)in, l.W, B, K, O, dense_fwd_stream_splits(B, K, O, net->num_sms),
+                                  net->ws, st);
       } else if (dense_fwd_simt_enabled()) {
         splits = dense_fwd_simt_splits(B, K, O, net->num_sms);
         while (splits > 1 && (size_t)splits * B * O * 4 > net->ws_bytes) --splits;
@@ -579,6 +585,13 @@ int enqueue_backward(ce_net* net, int n, float lr, float mu) {
                                 : dense_dx_split3(g, l.W, B, K, O, (const float*)nullptr, (float*)gout,
                                                   net->num_sms, st);
             if (s != CE_OK) return s;
+            goto dx_done;
+          }
+          if (dense_stream_enabled(B, K, (long long)K * O)) {  // streaming-W FFMA
+            if (l.in_is_act)
+              dense_dx_stream(g, l.W, B, K, O, mask, (float*)gout, st);
+            else
+              dense_dx_stream(g, l.W, B, K, O, (const float*)nullptr, (float*)gout, st);
             goto dx_done;
           }
         }
@@ -1044,6 +1057,10 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         int spt = dense_fwd_splits(l.out_units, l.in_units, net->num_sms);
         ws = std::max(ws, (size_t)spt * B * l.out_units * 4);
       }
+      if (precision == CE_PREC_FP32 && dense_stream_enabled(1, l.in_units, (long long)l.in_units * l.out_units))
+        for (int bq : {(int)B, std::min((int)B, 64), std::min((int)B, 32), std::min((int)B, 16)})
+          ws = std::max(ws, (size_t)dense_fwd_stream_splits(bq, l.in_units, l.out_units, net->num_sms) * bq *
+                                l.out_units * 4);
       if (precision == CE_PREC_FP32 && dense_split3_enabled(1, (long long)l.in_units * l.out_units))
         ws = std::max(ws, (size_t)dense_fwd_split3_splits(l.out_units, l.in_units, net->num_sms) * B * l.out_units * 4);
       long long bps = simt_tiles((int)B, l.out_units);
@@ -1067,7 +1084,10 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
         ws = std::max(ws, (size_t)sp * l.g.co * K * 4 + (size_t)(kColsumMaxSplits + 64) * l.g.co * 4);
         if (net->use_tc) {  // split-K partials of a sub-wave forward, for any batch the net may run
           ConvGeom gb = l.g;
-          for (gb.n = 1; gb.n <= (int)B; ++gb.n) ws = std::max(ws, conv_fwd_ws_bytes(gb, net->num_sms));
+          const Layer* pool = i + 1 < net->L.size() && net->L[i + 1].fused ? &net->L[i + 1] : nullptr;
+          for (gb.n = 1; gb.n <= (int)B; ++gb.n)
+            ws = std::max(ws, pool ? conv_pool_ws_bytes(gb, pool->g.k, pool->g.s, net->num_sms)
+                                   : conv_fwd_ws_bytes(gb, net->num_sms));
         }
         l.col2im = net->use_tc && l.need_dx && col2im_dgrad_eligible(l.g);
         if (l.col2im) zbytes = std::max(zbytes, col2im_dgrad_zbytes(l.g, (int)B));

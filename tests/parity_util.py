@@ -48,6 +48,11 @@ CASES = [
     ("fused_norelu_c64", "id=case0000000008 " + _BASE +
      "f0=conv:oc=64,k=5,s=1,relu=0 f1=pool:size=2,s=2 f2=conv:oc=128,k=3,s=1,relu=1 f3=pool:size=3,s=3",
      (3, 40, 40)),
+    # sub-wave layers (few tiles, long K): split-K forward with the pooled reduce (f1 + f2) and
+    # with the plain bias/ReLU reduce (f3)
+    ("subwave_splitk", "id=case0000000010 " + _BASE +
+     "f0=conv:oc=96,k=4,s=2,relu=1 f1=conv:oc=128,k=4,s=1,relu=1 f2=pool:size=2,s=2 "
+     "f3=conv:oc=64,k=3,s=1,relu=1", (3, 40, 40)),
     # C2 population genome #15 (2d5ebb4eae1bf684): 262,144 -> 523 head
     ("c2_g15", "id=2d5ebb4eae1bf684 parents= lr=0.017072315886796932 momentum=0.5 batch_size=32 "
      "f0=conv:oc=256,k=5,s=3,relu=1 h0=dense:units=523", (3, 100, 100)),
