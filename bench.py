@@ -68,6 +68,8 @@ def parse_args():
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="run only the per-kernel profiling pass (for an ncu capture of the same launch mix)")
+    ap.add_argument("--profile-batches", type=int, default=None,
+                    help="with --profile-only: batches per epoch (one epoch); the per-step launch mix is the same")
     return ap.parse_args()
 
 
@@ -313,10 +315,11 @@ def main():
     generation = [0]
     last_report = [None]
 
-    def step(profile=False):
+    def step(profile=False, pbudget=None):
         if profile:  # serial per-kernel profiling pass over the base generation (same genomes every rank)
             base = genomes[:POP_PER_GPU] if args.workload == "c2" else genomes
-            recs, _ = evaluate_population(base, splits, budget, obj, seed=0, devices=(device,), slots_per_gpu=1,
+            recs, _ = evaluate_population(base, splits, pbudget or budget, obj, seed=0, devices=(device,),
+                                          slots_per_gpu=1,
                                           precision=args.precision, profile=True, order="lpt")
             return recs
         generation[0] += 1
@@ -327,10 +330,16 @@ def main():
         last_report[0] = report
         return recs
 
-    if args.profile_only:
-        step()
-        step(profile=True)
+    if args.profile_only:  # one profiling pass; prints the bracket count per class (ncu traffic denominators)
+        pb = TrainBudget(epochs=1, max_batches_per_epoch=args.profile_batches) if args.profile_batches else None
+        recs = step(profile=True, pbudget=pb)
         torch.cuda.synchronize()
+        counts = {}
+        for r in recs:
+            for name, vals in (r.extras.get("kernel_profile", {}) if r is not None and r.ok else {}).items():
+                counts[name] = counts.get(name, 0) + int(vals[0])
+        print(json.dumps({"profile_only": True, "class_launches": counts,
+                          "ok": sum(1 for r in recs if r is not None and r.ok), "candidates": len(recs)}))
         return 0
 
     def timed(n_steps, e2e=False):

@@ -40,12 +40,17 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+TRACE_LIB_PATH = os.path.join(LIB_DIR, "libmenndl_sm100_trace.so")  # -DCE_TC_TRACE debug build (tools/tc_trace.py)
+
+
+def build(force=False, verbose=False, trace=False):
+    out = TRACE_LIB_PATH if trace else LIB_PATH
+    if not force and not trace and up_to_date():
         return LIB_PATH
     os.makedirs(LIB_DIR, exist_ok=True)
     cmd = [nvcc_path(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC",
-           "-I", os.path.join(ROOT, "include"), "-o", LIB_PATH + ".tmp",
+           *(["-DCE_TC_TRACE"] if trace else []),
+           "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -56,9 +61,9 @@ def build(force=False, verbose=False):
         raise RuntimeError("nvcc failed building libmenndl_sm100.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -96,6 +96,85 @@ inline bool make_tmap_im2col(CUtensorMap* map, const bf16* x, const ConvGeom& g,
   return true;
 }
 
+// Output tiles as 2-D pixel blocks (stride-1 convolutions): a 128-row GEMM tile
+// is a BH x BW block of output pixels of one image, rows row-major inside it,
+// so the A operand of every (tap, 64-channel slab) is ONE tiled TMA box of the
+// input {64 ch, BW, BH, 1} at the block origin shifted by the tap. The im2col
+// TMA mode moves a 128-pixel column at ~7 SM cycles per pixel row (measured,
+// tools/tc_trace.py), which capped every im2col k-block at ~900 cycles; tiled
+// boxes stream at the TMA's full rate. Rows past the map edge are computed on
+// zero-filled / neighbouring input and never stored.
+struct PixelBlocks {
+  int bh, bw_log2, oh, ow, n;
+  FastDiv d_bw_tiles, d_bh_tiles;  // blocks per image row / column
+  // block origin of tile t = m0 / 128; false past the last block
+  __device__ __forceinline__ bool origin(int m0, int& img, int& p0, int& q0) const {
+    uint32_t rest, qb, nn, pb;
+    d_bw_tiles.divmod((uint32_t)m0 >> 7, rest, qb);
+    d_bh_tiles.divmod(rest, nn, pb);
+    img = (int)nn;
+    p0 = (int)pb * bh;
+    q0 = (int)qb << bw_log2;
+    return img < n;
+  }
+  // output pixel index of row `row` of the tile at m0, or -1
+  __device__ __forceinline__ int pixel(int m0, int row) const {
+    int img, p0, q0;
+    if (!origin(m0, img, p0, q0)) return -1;
+    const int p = p0 + (row >> bw_log2), q = q0 + (row & ((1 << bw_log2) - 1));
+    return (p < oh && q < ow) ? (img * oh + p) * ow + q : -1;
+  }
+};
+// block shape minimising the padded tile count (ties: wider rows)
+inline PixelBlocks make_pixel_blocks(int n, int oh, int ow) {
+  PixelBlocks b{};
+  long long best = -1;
+  for (int l = 7; l >= 3; --l) {
+    const int bw = 1 << l, bh = TC_BM / bw;
+    const long long cost = (long long)((oh + bh - 1) / bh) * ((ow + bw - 1) / bw);
+    if (best < 0 || cost < best) {
+      best = cost;
+      b.bw_log2 = l;
+      b.bh = bh;
+    }
+  }
+  b.oh = oh;
+  b.ow = ow;
+  b.n = n;
+  b.d_bw_tiles = FastDiv((uint32_t)((ow + (1 << b.bw_log2) - 1) >> b.bw_log2));
+  b.d_bh_tiles = FastDiv((uint32_t)((oh + b.bh - 1) / b.bh));
+  return b;
+}
+inline int pixel_block_tiles(const PixelBlocks& b) {
+  return b.n * ((b.oh + b.bh - 1) / b.bh) * ((b.ow + (1 << b.bw_log2) - 1) >> b.bw_log2);
+}
+// tiled 4-D map over an NHWC bf16 tensor: boxes {64 channels, bw, bh, 1}, SWIZZLE_128B
+inline bool make_tmap_blocks(CUtensorMap* map, const bf16* x, int n, int h, int w, int c, int bh, int bw) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)x, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// CE_PIXEL_BLOCKS=1 (opt-in): measured no faster than the im2col TMA once the MMA
+// issue was made warp-converged, and the padded blocks waste rows on small maps
+inline bool pixel_blocks_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CE_PIXEL_BLOCKS");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 inline bool tma_disabled() {
   const char* e = getenv("CE_DISABLE_TMA");
   return e && e[0] == '1';
@@ -184,6 +263,10 @@ struct FwdTcLoader {
   PoolMap pm;  // POOL
   static_assert(!POOL || MODE <= 1, "the pooled row order needs the gather loader");
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
+    if ((IM2COL || NARROW) && tid == 0) {
+      tma_prefetch_desc(&wmap);
+      tma_prefetch_desc(&xmap);
+    }
     if (IM2COL || NARROW) return;
     int* xoff = (int*)table;
     for (int k8 = tid; k8 < K / 8; k8 += nthreads) {
@@ -271,6 +354,72 @@ struct FwdTcLoader {
   }
 };
 
+// Stride-1 forward over pixel blocks (PixelBlocks): per k-block one tiled box
+// of x at (c0, q0 + j, p0 + i, img) and one weight box. PAIR: the CTA-pair
+// variant (rank r takes block 2t + r and weight rows n0 + r BN / 2; copies
+// complete on rank 0's barrier).
+template <bool PAIR>
+struct FwdBlockLoader {
+  static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true;
+  CUtensorMap wmap;  // box 64 K x (PAIR ? BN / 2 : BN) rows
+  CUtensorMap xmap;  // make_tmap_blocks
+  PixelBlocks pb;
+  int cin, k, BN;
+  __device__ void init(uint8_t*, int tid, int) const {
+    if (tid == 0) {
+      tma_prefetch_desc(&wmap);
+      tma_prefetch_desc(&xmap);
+    }
+  }
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
+                       uint64_t* full) const {
+    const int cpb = cin / 64;
+    const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
+    const int i = tap / k, j = tap - i * k;
+    int img, p0, q0;
+    pb.origin(c.m0, img, p0, q0);
+    if constexpr (PAIR) {
+      const uint32_t rank = cluster_ctarank();
+      if (rank == 0) mbar_expect_tx(full, (uint32_t)(2 * TC_BM + BN) * 128u);
+      tma_load_4d_pair(sA, &xmap, c0, q0 + j, p0 + i, img, full);
+      tma_load_2d_pair(sB, &wmap, kb * TC_BK, c.n0 + (int)rank * (BN / 2), full);
+    } else {
+      mbar_expect_tx(full, (uint32_t)(TC_BM + BN) * 128u);
+      tma_load_4d(sA, &xmap, c0, q0 + j, p0 + i, img, full);
+      tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+    }
+  }
+};
+
+// CTA-pair forward loader (tc_gemm_kernel<..., PAIR = true>): the im2col TMA of
+// FwdTcLoader<2> for this CTA's 128 rows, and B rows n0 + rank * BN / 2 (a
+// BN / 2-row weight box); every copy completes on rank 0's barrier, which
+// rank 0 primes with the pair's total bytes.
+struct FwdTcLoaderPair {
+  static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true;
+  CUtensorMap wmap;  // box: 64 K x BN / 2 rows
+  CUtensorMap xmap;  // im2col, 128 pixels x 64 channels
+  ConvGeom g;
+  int K, M, BN;
+  FastDiv d_ow, d_oh;
+  __device__ void init(uint8_t*, int, int) const {}
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
+                       uint64_t* full) const {
+    const uint32_t rank = cluster_ctarank();
+    const int cpb = g.c / 64;
+    const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
+    const int i = tap / g.k, j = tap - i * g.k;
+    uint32_t q, p, n, t;
+    d_ow.divmod((uint32_t)c.m0, t, q);
+    d_oh.divmod(t, n, p);
+    if (rank == 0) mbar_expect_tx(full, (uint32_t)(2 * TC_BM + BN) * 128u);
+    tma_load_im2col_4d_pair(sA, &xmap, c0, (int)q * g.s, (int)p * g.s, (int)n, (uint16_t)j, (uint16_t)i, full);
+    tma_load_2d_pair(sB, &wmap, kb * TC_BK, c.n0 + (int)rank * (BN / 2), full);
+  }
+};
+
 struct FwdTcEpi {
   static constexpr bool STAGED_BF16 = true;  // coalesced row stores through shared memory (tc_engine)
   // pure-TMA loaders (1 producer warp) leave room for 16 epilogue warps: the bf16
@@ -280,6 +429,12 @@ struct FwdTcEpi {
   bf16* y;
   const float* bias;
   int M, co, relu;
+  PixelBlocks pb{};  // pb.bh > 0: rows are pixel blocks (FwdBlockLoader), else m = m0 + row
+  __device__ __forceinline__ int row_pixel(const TileCoord& c, int row) const {
+    if (pb.bh > 0) return pb.pixel(c.m0, row);
+    const int m = c.m0 + row;
+    return m < M ? m : -1;
+  }
   // bias + ReLU of columns c.n0 + col .. +15 (row independent)
   // out[i] = bf16x2 of columns 2i, 2i+1
   __device__ void convert(const TileCoord& c, int col, const float (&v)[16], uint32_t (&out)[8]) const {
@@ -308,13 +463,13 @@ struct FwdTcEpi {
   }
   // destination of the 8-column half `half` of row `row` at columns col.., or null
   __device__ bf16* row_ptr(const TileCoord& c, int row, int col, int half) const {
-    const int m = c.m0 + row, o = c.n0 + col + half * 8;
-    return (m < M && o < co) ? y + (size_t)m * co + o : nullptr;
+    const int m = row_pixel(c, row), o = c.n0 + col + half * 8;
+    return (m >= 0 && o < co) ? y + (size_t)m * co + o : nullptr;
   }
   __device__ void store(const TileCoord& c, int row, int col, const float (&v)[16]) const {
-    const int m = c.m0 + row;
+    const int m = row_pixel(c, row);
     const int o0 = c.n0 + col;
-    if (m >= M || o0 >= co) return;
+    if (m < 0 || o0 >= co) return;
     bf16* dst = y + (size_t)m * co + o0;
     __align__(16) bf16 out[16];
 #pragma unroll
@@ -570,6 +725,34 @@ inline bool make_tmap_im2col_dgrad(CUtensorMap* map, const bf16* dy, const ConvG
   return true;
 }
 
+// CTA-pair dgrad loader (one sub-pixel class): FwdTcLoaderPair's scheme over the
+// class's im2col view of dY and its weight block
+struct DgradTcLoaderPair {
+  static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true;
+  CUtensorMap wmap;  // class block [c][K], box 64 K x BN / 2 rows
+  CUtensorMap dmap;
+  ConvGeom g;
+  DgradClass cl;
+  int K, M, BN;
+  FastDiv d_wc, d_hc;
+  __device__ void init(uint8_t*, int, int) const {}
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
+                       uint64_t* full) const {
+    const uint32_t rank = cluster_ctarank();
+    const int cpb = g.co / 64;
+    const int tap = kb / cpb, o0 = (kb - tap * cpb) * 64;
+    const int ap = tap / cl.tj, bp = tap - ap * cl.tj;
+    uint32_t ww, hh, n, t;
+    d_wc.divmod((uint32_t)c.m0, t, ww);
+    d_hc.divmod(t, n, hh);
+    if (rank == 0) mbar_expect_tx(full, (uint32_t)(2 * TC_BM + BN) * 128u);
+    tma_load_im2col_4d_pair(sA, &dmap, o0, (int)ww - (cl.tj - 1), (int)hh - (cl.ti - 1), (int)n, (uint16_t)bp,
+                            (uint16_t)ap, full);
+    tma_load_2d_pair(sB, &wmap, kb * TC_BK, c.n0 + (int)rank * (BN / 2), full);
+  }
+};
+
 struct DgradTcEpi {
   bf16* dx;
   const bf16* mask;
@@ -717,6 +900,35 @@ inline int pick_bn(int m_tiles, int n, int num_sms) {
   return bn;
 }
 
+// CTA-pair forward (cta_group::2, FwdTcLoaderPair): im2col-TMA layers (C % 64 == 0)
+// with N >= 128 and at least one 256-row tile per pair of SMs. CE_CONV_PAIR=0
+// keeps every forward on single-CTA tiles.
+inline bool conv_pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CE_CONV_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// Measured (conv_bench, r02 notes): pairs win on large maps with N = 256 (SWEET fwd
+// 1,407 -> 1,563 TF/s, dgrad 1,358 -> 1,460) and lose on the VGG16STYLE layers
+// (<= 1.4 waves of pair tiles, or N = 128), so: N > 128 and >= 4 waves of pair tiles.
+inline bool conv_pair_shape_ok(long long M, int n_cols, int num_sms) {
+  const long long pair_tiles = (M + 2 * TC_BM - 1) / (2 * TC_BM);
+  return n_cols > 128 && pair_tiles >= 4LL * (num_sms / 2);
+}
+inline bool conv_pair_ok(const ConvGeom& g, int num_sms) {
+  const long long M = (long long)g.n * g.oh * g.ow;
+  return conv_pair_enabled() && !tma_disabled() && !im2col_disabled() && g.c % 64 == 0 &&
+         conv_pair_shape_ok(M, g.co, num_sms);
+}
+// N width of a pair tile (128 or 256) by the same wave-quantised cost as pick_bn over SM pairs
+inline int pick_bn_pair(int m_tiles, int n, int num_sms) {
+  (void)m_tiles;
+  (void)num_sms;
+  return n > 128 ? 256 : 128;
+}
+
 template <class Fn>
 inline int with_bn(int n, Fn&& fn) {
   if (n <= 16) return fn(std::integral_constant<int, 16>());
@@ -838,6 +1050,57 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
       e = cudaGetLastError();
       return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_reduce: %s", cudaGetErrorString(e));
     });
+  }
+  if (pixel_blocks_enabled() && g.s == 1 && g.c % 64 == 0 && !tma_disabled() && !im2col_disabled()) {
+    // stride 1: pixel-block tiles, tiled TMA boxes (CTA pairs when wide and large enough)
+    const PixelBlocks pbk = make_pixel_blocks(g.n, g.oh, g.ow);
+    const int tiles = pixel_block_tiles(pbk);
+    const bool pair = conv_pair_enabled() && conv_pair_shape_ok((long long)tiles * TC_BM, g.co, num_sms);
+    auto go = [&](auto bnc, auto pairc) -> int {
+      constexpr int BN = decltype(bnc)::value;
+      constexpr bool P = decltype(pairc)::value;
+      FwdBlockLoader<P> ld{};
+      if (!make_tmap_kmajor(&ld.wmap, w, g.co, K, P ? BN / 2 : BN) ||
+          !make_tmap_blocks(&ld.xmap, x, g.n, g.h, g.w, g.c, pbk.bh, 1 << pbk.bw_log2))
+        return -1;
+      ld.pb = pbk; ld.cin = g.c; ld.k = g.k; ld.BN = BN;
+      FwdTcEpi ep{y, bias, M, g.co, relu};
+      ep.pb = pbk;
+      TcShape sh = tc_make_shape(tiles * TC_BM, g.co, K, BN, 1);
+      cudaError_t e;
+      if constexpr (P) {
+        sh.m_tiles = (tiles + 1) / 2;
+        e = tc_launch_pair<BN>(ld, ep, sh, num_sms, st);
+      } else {
+        e = tc_launch<BN>(ld, ep, sh, num_sms, st);
+      }
+      return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc blocks: %s", cudaGetErrorString(e));
+    };
+    int r;
+    if (pair) {
+      const int bn = pick_bn_pair((tiles + 1) / 2, g.co, num_sms);
+      r = bn == 256 ? go(std::integral_constant<int, 256>(), std::true_type())
+                    : go(std::integral_constant<int, 128>(), std::true_type());
+    } else {
+      r = with_bn(pick_bn(tiles, g.co, num_sms), [&](auto bn) { return go(bn, std::false_type()); });
+    }
+    if (r >= 0) return r;
+  }
+  if (conv_pair_ok(g, num_sms)) {  // CTA-pair M=256 tiles over the im2col TMA path
+    const int bn = pick_bn_pair((M + 2 * TC_BM - 1) / (2 * TC_BM), g.co, num_sms);
+    auto go = [&](auto bnc) -> int {
+      constexpr int BN = decltype(bnc)::value;
+      FwdTcLoaderPair ld{};
+      if (!make_tmap_kmajor(&ld.wmap, w, g.co, K, BN / 2) || !make_tmap_im2col(&ld.xmap, x, g, TC_BM)) return -1;
+      ld.g = g; ld.K = K; ld.M = M; ld.BN = BN;
+      ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
+      sh.m_tiles = (M + 2 * TC_BM - 1) / (2 * TC_BM);
+      cudaError_t e = tc_launch_pair<BN>(ld, FwdTcEpi{y, bias, M, g.co, relu}, sh, num_sms, st);
+      return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_fwd_tc pair: %s", cudaGetErrorString(e));
+    };
+    const int r = bn == 256 ? go(std::integral_constant<int, 256>()) : go(std::integral_constant<int, 128>());
+    if (r >= 0) return r;
   }
   return with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.co, num_sms), [&](auto bn) {
     cudaError_t e = launch(bn, FwdTcEpi{y, bias, M, g.co, relu}, 1);
@@ -1045,6 +1308,27 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
       if (cl.ti == 0 || cl.tj == 0) continue;
       const int M = g.n * cl.hc * cl.wc, K = cl.ti * cl.tj * g.co;
       if ((K / 8) * 12 > TC_TABLE_BYTES) return fail(CE_EINVAL, "conv_dgrad_tc: K=%d exceeds the chunk table", K);
+      if (conv_pair_enabled() && !tma_disabled() && !im2col_disabled() && g.co % 64 == 0 &&
+          conv_pair_shape_ok(M, g.c, num_sms)) {  // CTA-pair M=256 tiles
+        const bf16* wcls = wt + dg_class_base(g.k, g.s, g.c, g.co, rh * g.s + rw);
+        auto go = [&](auto bnc) -> int {
+          constexpr int BN = decltype(bnc)::value;
+          DgradTcLoaderPair ld{};
+          if (!make_tmap_kmajor(&ld.wmap, wcls, g.c, K, BN / 2) || !make_tmap_im2col_dgrad(&ld.dmap, dy, g, cl))
+            return -1;
+          ld.g = g; ld.cl = cl; ld.K = K; ld.M = M; ld.BN = BN;
+          ld.d_wc = FastDiv(cl.wc); ld.d_hc = FastDiv(cl.hc);
+          TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
+          sh.m_tiles = (M + 2 * TC_BM - 1) / (2 * TC_BM);
+          DgradTcEpi ep{dx, mask, g, cl, M, FastDiv(cl.wc), FastDiv(cl.hc)};
+          cudaError_t e = tc_launch_pair<BN>(ld, ep, sh, num_sms, st);
+          return e == cudaSuccess ? CE_OK : fail(CE_ECUDA, "conv_dgrad_tc pair: %s", cudaGetErrorString(e));
+        };
+        const int bnp = pick_bn_pair((M + 2 * TC_BM - 1) / (2 * TC_BM), g.c, num_sms);
+        const int r = bnp == 256 ? go(std::integral_constant<int, 256>()) : go(std::integral_constant<int, 128>());
+        if (r > 0) return r;
+        if (r == 0) continue;
+      }
       int s = with_bn(pick_bn((M + TC_BM - 1) / TC_BM, g.c, num_sms), [&](auto bn) {
         constexpr int BN = decltype(bn)::value;
         TcShape sh = tc_make_shape(M, g.c, K, BN, 1);

@@ -435,3 +435,16 @@ int ce_permute_flatten_weights(const float* src, size_t rows, int c, int c_store
 }
 
 }  // extern "C"
+
+#ifdef CE_TC_TRACE
+extern "C" int ce_debug_fake_load(int on) {
+  return cudaMemcpyToSymbol(ce::g_tc_fake_load, &on, sizeof(int)) == cudaSuccess ? CE_OK : CE_ECUDA;
+}
+// debug builds only (tools/tc_trace.py): copy and reset the tc_engine event trace
+extern "C" int ce_debug_trace(unsigned long long* out, unsigned int* counts) {
+  if (cudaMemcpyFromSymbol(out, ce::g_tc_trace, sizeof(ce::g_tc_trace)) != cudaSuccess) return CE_ECUDA;
+  if (cudaMemcpyFromSymbol(counts, ce::g_tc_trace_n, sizeof(ce::g_tc_trace_n)) != cudaSuccess) return CE_ECUDA;
+  static const unsigned int zero[4][3] = {};
+  return cudaMemcpyToSymbol(ce::g_tc_trace_n, zero, sizeof(zero)) == cudaSuccess ? CE_OK : CE_ECUDA;
+}
+#endif

@@ -16,6 +16,7 @@
 #include <condition_variable>
 #include <map>
 #include <mutex>
+#include <nvtx3/nvToolsExt.h>
 #include "ops.cuh"
 #include "conv_tc.cuh"
 #include "dense_tc.cuh"
@@ -110,6 +111,7 @@ static double g_peak_flops = 1.3877e15, g_peak_bytes = 6.5504e12;
 struct ce_net {
   int device = 0, prec = CE_PREC_BF16, num_sms = 148;
   bool prof_on = false;
+  bool prof_in_train = false;  // NVTX class ranges only around ce_train's own steps (what prof_collect counts)
   bool prof_capturing = false;  // Prof events become event-record nodes of the captured step graph
   std::vector<ProfEvent> prof_pending;
   ProfTotals prof[P_NCLASS];
@@ -244,11 +246,33 @@ struct ExclusiveGate {
   }
 };
 
+// How host threads wait on the device (CE_HOST_SYNC=spin|yield|blocking; unset
+// keeps the driver default, which spins while a process has one context). One
+// process per GPU with several slot threads each spinning in
+// cudaEventSynchronize can oversubscribe the host cores at N GPUs; blocking
+// sync parks the waiting threads instead. Applied once per device.
+static void apply_host_sync(int d) {
+  static std::atomic<unsigned long long> done{0};
+  if (d < 0 || d >= 64 || (done.load() >> d) & 1ull) return;
+  done.fetch_or(1ull << d);
+  const char* e = getenv("CE_HOST_SYNC");
+  if (!e || !e[0]) return;
+  unsigned flag = !strcmp(e, "blocking") ? cudaDeviceScheduleBlockingSync
+                  : !strcmp(e, "yield")  ? cudaDeviceScheduleYield
+                  : !strcmp(e, "spin")   ? cudaDeviceScheduleSpin
+                                         : cudaDeviceScheduleAuto;
+  unsigned cur = 0;
+  cudaGetDeviceFlags(&cur);
+  cudaSetDeviceFlags((cur & ~cudaDeviceScheduleMask) | flag);
+  cudaGetLastError();
+}
+
 struct DevGuard {
   int prev = -1;
   explicit DevGuard(int d) {
     cudaGetDevice(&prev);
     if (prev != d) cudaSetDevice(d);
+    apply_host_sync(d);
   }
   ~DevGuard() {
     int cur;
@@ -292,6 +316,14 @@ void keep_pool_memory(int device) {
   }
 }
 
+// CE_PROF_NVTX=1: the profiling pass runs eagerly and each class bracket is also
+// an NVTX push/pop range named after the class, so `ncu --nvtx --nvtx-include
+// dense_bwd/` measures DRAM bytes on exactly the launches the events time.
+static bool prof_nvtx() {
+  static const bool on = [] { const char* e = getenv("CE_PROF_NVTX"); return e && e[0] == '1'; }();
+  return on;
+}
+
 struct Prof {
   ce_net* net;
   int cls;
@@ -304,6 +336,7 @@ struct Prof {
     if (net->prof_on) {
       cudaEventCreate(&a);
       cudaEventRecordWithFlags(a, net->st, net->prof_capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+      if (prof_nvtx() && net->prof_in_train) nvtxRangePushA(kProfNames[cls]);
     }
   }
   ~Prof() {
@@ -312,6 +345,7 @@ struct Prof {
       cudaEventCreate(&b);
       cudaEventRecordWithFlags(b, net->st, net->prof_capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
       net->prof_pending.push_back(ProfEvent{cls, layer, flops, bytes, a, b});
+      if (prof_nvtx() && net->prof_in_train) nvtxRangePop();
     }
   }
 };
@@ -1455,7 +1489,7 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   long long per_step = 0;
   SharedGate capture_gate(net->device);  // no exclusive latency window (device sync) during a capture
   if (net->prof_on) prof_release(net);
-  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+  if (!(net->prof_on && prof_nvtx()) && cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
     cudaGraph_t graph = nullptr;
     net->prof_capturing = net->prof_on;
     int s = gather_any(net, ds, net->d_perm, n_perm, steps_per_epoch, 0, batch, true);
@@ -1490,6 +1524,11 @@ int ce_train(ce_net* net, const ce_dataset* ds, const int32_t* perm, int n_perm,
   // (the reference stops at the first non-finite loss, evaluator.py:168-170).
   const int chunk = 16;
   int launched = 0, nchunk = 0;
+  struct InTrain {  // NVTX class ranges of the eager profiling pass: this loop's steps only
+    ce_net* n;
+    explicit InTrain(ce_net* x) : n(x) { n->prof_in_train = true; }
+    ~InTrain() { n->prof_in_train = false; }
+  } in_train(net);
   while (launched < steps) {
     const int todo = std::min(chunk, steps - launched);
     {

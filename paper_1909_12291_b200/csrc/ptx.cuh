@@ -38,6 +38,25 @@ CE_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// wait with cluster-scope acquire: the phase was completed by arrivals from the peer CTA
+CE_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+  }
+}
+// whole-warp wait with a warp-uniform exit (vote): code after it stays provably
+// converged, so the MMA warp's descriptor arithmetic can use the uniform datapath
+CE_DEV void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+  }
+}
 CE_DEV void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -56,6 +75,14 @@ CE_DEV void tma_load_2d(uint32_t dst, const void* tmap, int x, int y, uint64_t* 
       "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// tiled 4-D copy (NHWC box: channels x W x H x 1); out-of-range coordinates zero-fill
+CE_DEV void tma_load_4d(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+          "r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
 // im2col-mode 4-D copy (NHWC): `pixels_per_column` output pixels starting at the
 // receptive-field origin (c, w, h, n), shifted by the filter tap (off_w, off_h).
 CE_DEV void tma_load_im2col_4d(uint32_t dst, const void* tmap, int c, int w, int h, int n, uint16_t off_w,
@@ -66,6 +93,53 @@ CE_DEV void tma_load_im2col_4d(uint32_t dst, const void* tmap, int c, int w, int
       "l"(tmap), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar)), "h"(off_w), "h"(off_h)
       : "memory");
 }
+// ---------------------------------------------------------------- CTA pairs (cta_group::2)
+// Two CTAs of a (2,1,1) cluster on one TPC run one M=256 MMA: each holds its
+// 128 rows of A and half of B in shared memory and its 128 accumulator lanes in
+// TMEM; rank 0 issues the MMAs. The shared::cta address of a barrier with bit 24
+// cleared names the same barrier in rank 0 (the pair's peer bit).
+constexpr uint32_t kPairPeerMask = 0xFEFFFFFFu;
+CE_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+CE_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA `rank` of the cluster
+CE_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+// TMA copies into this CTA's shared memory whose bytes complete on rank 0's barrier
+CE_DEV void tma_load_2d_pair(uint32_t dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar) & kPairPeerMask)
+      : "memory");
+}
+CE_DEV void tma_load_4d_pair(uint32_t dst, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar) & kPairPeerMask)
+      : "memory");
+}
+CE_DEV void tma_load_im2col_4d_pair(uint32_t dst, const void* tmap, int c, int w, int h, int n, uint16_t off_w,
+                                    uint16_t off_h, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.im2col.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(tmap), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar) & kPairPeerMask), "h"(off_w), "h"(off_h)
+      : "memory");
+}
+
 CE_DEV void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
@@ -99,6 +173,15 @@ CE_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
 CE_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+CE_DEV void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+CE_DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
 CE_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 CE_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -109,6 +192,88 @@ CE_DEV void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// D[tmem, both CTAs] (+)= A[smem, 2 x 128 rows] * B[smem, 2 x N/2 rows]^T (rank 0 issues)
+CE_DEV void umma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive (once) on the barrier at this offset in both CTAs of the pair when the pair's MMAs complete
+CE_DEV void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// Warp-wide forms: the whole (converged) warp executes them with warp-uniform
+// operands and one lane, chosen by elect.sync, issues. Keeping the issuing code
+// converged lets the descriptors live in uniform registers; the lane-0-only
+// forms make the compiler wrap every tcgen05 op in an elect / R2UR broadcast
+// loop (~140 SM cycles per MMA measured, tools/tc_trace.py).
+CE_DEV void umma_bf16_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+CE_DEV void umma_bf16_pair_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Four K=16 steps of one 64-deep k-block in one asm block (warp-wide, elected
+// lane issues): descriptors advance by a_step / b_step (address units of 16 B).
+#define CE_UMMA4_BODY(CG)                                                                          \
+  "{\n\t.reg .pred e, p0, p1;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"                           \
+  "elect.sync _|e, 0xffffffff;\n\t"                                                                \
+  "setp.ne.b32 p0, %4, 0;\n\t"                                                                     \
+  "setp.eq.u32 p1, 0, 0;\n\t"                                                                      \
+  "add.s64 a1, %1, %5;\n\tadd.s64 a2, a1, %5;\n\tadd.s64 a3, a2, %5;\n\t"                         \
+  "add.s64 b1, %2, %6;\n\tadd.s64 b2, b1, %6;\n\tadd.s64 b3, b2, %6;\n\t"                         \
+  "@e tcgen05.mma." CG ".kind::f16 [%0], %1, %2, %3, p0;\n\t"                                       \
+  "@e tcgen05.mma." CG ".kind::f16 [%0], a1, b1, %3, p1;\n\t"                                        \
+  "@e tcgen05.mma." CG ".kind::f16 [%0], a2, b2, %3, p1;\n\t"                                        \
+  "@e tcgen05.mma." CG ".kind::f16 [%0], a3, b3, %3, p1;\n\t}"
+CE_DEV void umma4_warp(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t accumulate,
+                       uint64_t a_step, uint64_t b_step) {
+  asm volatile(CE_UMMA4_BODY("cta_group::1")::"r"(d_tmem), "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate),
+               "l"(a_step), "l"(b_step)
+               : "memory");
+}
+CE_DEV void umma4_pair_warp(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t accumulate,
+                            uint64_t a_step, uint64_t b_step) {
+  asm volatile(CE_UMMA4_BODY("cta_group::2")::"r"(d_tmem), "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate),
+               "l"(a_step), "l"(b_step)
+               : "memory");
+}
+CE_DEV void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+CE_DEV void umma_commit_pair_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::
+          "r"(smem_u32(bar)),
+      "h"((uint16_t)3)
       : "memory");
 }
 // arrive (once) on an mbarrier when all previously issued tcgen05 ops complete

@@ -119,6 +119,30 @@ struct TcRoles {
   static constexpr int EPI_STAGE = EpiStaged<Epi>::value ? EW * 1024 : EW * EpiWarpSmem<Epi>::value;
 };
 constexpr int TC_TABLE_BYTES = 20480;              // loader lookup tables
+
+// Pipeline event trace (debug builds with -DCE_TC_TRACE, tools/tc_trace.py): the
+// first 4 CTAs record clock64 at every producer issue, MMA full-barrier pass and
+// epilogue drain, one region per role: [kind:4][tile:14][kb:14][clock:32].
+#ifdef CE_TC_TRACE
+__device__ unsigned long long g_tc_trace[4][3][4096];
+__device__ unsigned int g_tc_trace_n[4][3];
+// one recording thread per role: the index lives in a register, stores are fire-and-forget
+__device__ __forceinline__ void tc_trace(unsigned int& i, int role, int kind, int tile, int kb) {
+  if (blockIdx.x < 4 && i < 4096)
+    g_tc_trace[blockIdx.x][role][i] = ((unsigned long long)kind << 60) | ((unsigned long long)(tile & 0x3FFF) << 46) |
+                                      ((unsigned long long)(kb & 0x3FFF) << 32) | (clock64() & 0xFFFFFFFFull);
+  ++i;
+}
+__device__ __forceinline__ void tc_trace_done(unsigned int i, int role) {
+  if (blockIdx.x < 4) g_tc_trace_n[blockIdx.x][role] = i;
+}
+__device__ int g_tc_fake_load;  // 1: producers skip the copies (MMA / barrier rate without memory)
+#define TC_TRACE(role, kind, tile, kb) tc_trace(trace_i, role, kind, tile, kb)
+#define TC_TRACE_DONE(role) tc_trace_done(trace_i, role)
+#else
+#define TC_TRACE(role, kind, tile, kb) ((void)0)
+#define TC_TRACE_DONE(role) ((void)0)
+#endif
 constexpr int TC_MAX_LAG = 8;
 
 
@@ -170,10 +194,11 @@ __device__ inline TileCoord tc_tile(const TcShape& s, int t, int bn) {
   return c;
 }
 
-template <int BN, int EPI_STAGE = 0, int PLANES = 1>
+// BROWS: B rows held per CTA (BN, or BN / 2 for a CTA pair)
+template <int BN, int EPI_STAGE = 0, int PLANES = 1, int BROWS = BN>
 struct TcSmemLayout {
   static constexpr int A_PLANE = TC_BM * TC_BK * 2;  // 16 KB
-  static constexpr int B_PLANE = BN * TC_BK * 2;
+  static constexpr int B_PLANE = BROWS * TC_BK * 2;
   static constexpr int A_BYTES = A_PLANE * PLANES;
   static constexpr int B_BYTES = B_PLANE * PLANES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -189,14 +214,21 @@ struct TcSmemLayout {
   static constexpr int TOTAL = STAGES * STAGE_BYTES + TC_TABLE_BYTES + BAR_BYTES + EPI_STAGE + 1024;  // + slack
 };
 
-template <int BN, class Loader, class Epi>
+// PAIR: the CTA-pair variant (cta_group::2, launched as (2,1,1) clusters). A
+// tile is 256 rows x BN; rank r of the pair loads rows m0 + 128 r of A and B
+// rows n0 + r BN/2, rank 0 issues M=256 MMAs over both CTAs' shared memory and
+// each CTA drains its own 128 TMEM lanes. Per SM the B operand bytes read by the
+// tensor core per FLOP halve, which is what bounds BN <= 128 tiles on one SM.
+// Shape: m_tiles counts 256-row tiles. Pure-TMA loaders only.
+template <int BN, class Loader, class Epi, bool PAIR = false>
 __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ Loader ld, const __grid_constant__ Epi epi, const TcShape shape) {
   using R = TcRoles<Loader, Epi>;
   constexpr bool STAGED = EpiStaged<Epi>::value;
   constexpr int WSM = EpiWarpSmem<Epi>::value;
   constexpr bool SPLIT = Split3<Loader>::value;
-  using L = TcSmemLayout<BN, R::EPI_STAGE, SPLIT ? 3 : 1>;
+  static_assert(!PAIR || (Loader::PURE_TMA && !SPLIT && BN >= 32), "CTA pairs: pure-TMA loaders, BN >= 32");
+  using L = TcSmemLayout<BN, R::EPI_STAGE, SPLIT ? 3 : 1, PAIR ? BN / 2 : BN>;
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -211,6 +243,17 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int total_tiles = shape.m_tiles * shape.n_tiles * shape.splits;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+#ifdef CE_TC_TRACE
+  unsigned int trace_i = 0;
+#endif
+  const int tile0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // first tile / stride of this CTA (pair)
+  const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  auto tile_at = [&](int t) {
+    TileCoord c = tc_tile(shape, t, BN);
+    if (PAIR) c.m0 = c.m0 * 2 + (int)rank * TC_BM;
+    return c;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -219,14 +262,20 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], R::EW * 32);
+      mbar_init(&tempty[i], PAIR ? 2 * R::EW : R::EW * 32);  // pair: one arrival per epilogue warp of both CTAs
     }
     fence_barrier_init();
   }
-  if (warp == R::MMA_WARP) tmem_alloc(tmem_base_slot, L::TMEM_COLS);
+  if (warp == R::MMA_WARP) {
+    if constexpr (PAIR)
+      tmem_alloc_pair(tmem_base_slot, L::TMEM_COLS);
+    else
+      tmem_alloc(tmem_base_slot, L::TMEM_COLS);
+  }
   ld.init(table, threadIdx.x, R::THREADS);
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // the peer's barriers exist before any copy or commit targets them
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   const uint32_t smem_base = smem_u32(smem);
@@ -240,15 +289,21 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     uint32_t phase = 0;
     int pending_stage[TC_MAX_LAG + 1];
     int npending = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      TileCoord c = tc_tile(shape, t, BN);
+    for (int t = tile0; t < total_tiles; t += tstep) {
+      TileCoord c = tile_at(t);
       for (int kb = 0; kb < c.nkb; ++kb) {
+        if (threadIdx.x == 0) TC_TRACE(0, 1, t, kb);
         mbar_wait(&empty[stage], phase ^ 1);
+        if (threadIdx.x == 0) TC_TRACE(0, 2, t, kb);
         const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
         const uint32_t sB = sA + L::A_BYTES;
-        if (Loader::PURE_TMA) {  // copies complete on the barrier themselves
+        if (Loader::PURE_TMA) {  // copies complete on the barrier themselves (pair: rank 0's)
+#ifdef CE_TC_TRACE
+          if (!g_tc_fake_load)
+#endif
           ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
-          mbar_arrive(&full[stage]);
+          TC_TRACE(0, 7, t, kb);
+          if (!PAIR || rank == 0) mbar_arrive(&full[stage]);
         } else if constexpr (SyncFill<Loader>::value) {  // st.shared fill: visible to the MMA after the fence
           ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
           fence_proxy_async();
@@ -276,6 +331,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     cp_async_wait_all();
     fence_proxy_async();
     for (int i = 0; i < npending; ++i) mbar_arrive(&full[pending_stage[i]]);
+    if (threadIdx.x == 0) TC_TRACE_DONE(0);
   } else if (warp < R::MMA_WARP) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter (warp % 4 == q)
@@ -286,10 +342,11 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     const int col_end = col_begin + GCOLS < BN ? col_begin + GCOLS : BN;
     const int row_in_tile = q * 32 + lane;
     int lt = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++lt) {
-      TileCoord c = tc_tile(shape, t, BN);
+    for (int t = tile0; t < total_tiles; t += tstep, ++lt) {
+      TileCoord c = tile_at(t);
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      if (warp == R::PW && lane == 0) TC_TRACE(2, 5, t, 0);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * L::ACC_COLS);
       if constexpr (STAGED) {
@@ -353,35 +410,53 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
             epi.store(c, row_in_tile, col, v);
         }
       }
+      if (warp == R::PW && lane == 0) TC_TRACE(2, 6, t, 0);
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR) {  // one arrival per warp on rank 0's barrier
+        __syncwarp();
+        if (lane == 0) {
+          if (rank == 0)
+            mbar_arrive(&tempty[acc]);
+          else
+            mbar_arrive_cluster(&tempty[acc], 0);
+        }
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
     }
+    if (warp == R::PW && lane == 0) TC_TRACE_DONE(2);
     epi.finish(lane, q);
-  } else {
+  } else if (!PAIR || rank == 0) {
     // ------------------------------------------------------------ MMA issuer
     int stage = 0;
     uint32_t phase = 0;
     int lt = 0;
-    constexpr uint32_t idesc = make_idesc_bf16(TC_BM, BN, Loader::A_MN_MAJOR, Loader::B_MN_MAJOR);
+    constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * TC_BM : TC_BM, BN, Loader::A_MN_MAJOR, Loader::B_MN_MAJOR);
     const int k16_total = (shape.K + 15) / 16;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++lt) {
-      TileCoord c = tc_tile(shape, t, BN);
+    for (int t = tile0; t < total_tiles; t += tstep, ++lt) {
+      TileCoord c = tile_at(t);
       const int acc = lt & 1;
-      mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+      if constexpr (PAIR)
+        mbar_wait_cluster(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+      else
+        mbar_wait_warp(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+      __syncwarp();
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * L::ACC_COLS);
+      if (lane == 0) TC_TRACE(1, 4, t, 0);
       for (int kb = 0; kb < c.nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait_warp(&full[stage], phase);
+        if (lane == 0) TC_TRACE(1, 3, t, kb);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
-          const uint32_t sB = sA + L::A_BYTES;
-          const int gkb = c.kb0 + kb;
-          int nk16 = k16_total - gkb * (TC_BK / 16);
-          if (nk16 > TC_BK / 16) nk16 = TC_BK / 16;
+        const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
+        const uint32_t sB = sA + L::A_BYTES;
+        const int gkb = c.kb0 + kb;
+        int nk16 = k16_total - gkb * (TC_BK / 16);
+        if (nk16 > TC_BK / 16) nk16 = TC_BK / 16;
+        if constexpr (SPLIT) {
+          if (lane == 0) {
 #pragma unroll 1
-          for (int k = 0; k < nk16; ++k) {
-            if constexpr (SPLIT) {
+            for (int k = 0; k < nk16; ++k) {
               // six plane products (no-swizzle canonical layouts): the five cross terms,
               // smallest first, into a second accumulator so the hi*hi chain (the large
               // one) takes a single accumulation per K=16 step; the epilogue adds the two
@@ -396,26 +471,49 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
                 umma_bf16(d_tmem + (big ? 0u : (uint32_t)BN), ad, bd, idesc,
                           (kb > 0 || k > 0 || (!big && q > 0)) ? 1u : 0u);
               }
-              continue;
             }
-            // K-major: a K=16 step covers chunks 2k, 2k+1 (LBO apart).
-            // MN-major: a K=16 step covers K groups 2k, 2k+1 (LBO apart).
-            uint64_t ad;
-            if (Loader::A_TMA_SW128)
-              ad = Loader::A_MN_MAJOR ? make_sdesc_sw128_mn(sA + (uint32_t)k * 2048, 64 * 128)
-                                      : make_sdesc_sw128(sA + (uint32_t)k * 32);
-            else
-              ad = make_sdesc(sA + (uint32_t)(2 * k) * (TC_BM * 16), TC_BM * 16, 128);
-            uint64_t bd;
-            if (Loader::B_TMA_SW128)
-              bd = Loader::B_MN_MAJOR ? make_sdesc_sw128_mn(sB + (uint32_t)k * 2048, 64 * 128)
-                                      : make_sdesc_sw128(sB + (uint32_t)k * 32);
-            else
-              bd = make_sdesc(sB + (uint32_t)(2 * k) * (BN * 16), BN * 16, 128);
-            umma_bf16(d_tmem, ad, bd, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&empty[stage]);
+            if (kb == c.nkb - 1) umma_commit(&tfull[acc]);
           }
-          umma_commit(&empty[stage]);
-          if (kb == c.nkb - 1) umma_commit(&tfull[acc]);
+        } else {
+          // warp-converged issue (umma_*_warp): descriptors at K step 0, advanced linearly.
+          // K-major SW128: +32 B per K=16 step; MN-major SW128: +2 K groups (2048 B);
+          // no-swizzle K-major: +2 chunk columns (2 x rows x 16 B). Descriptor address field = bytes >> 4.
+          constexpr uint32_t A_STEP = Loader::A_TMA_SW128 ? (Loader::A_MN_MAJOR ? 2048u : 32u) : 2u * TC_BM * 16u;
+          constexpr uint32_t B_STEP = Loader::B_TMA_SW128 ? (Loader::B_MN_MAJOR ? 2048u : 32u) : 2u * BN * 16u;
+          const uint64_t ad0 = Loader::A_TMA_SW128
+                                   ? (Loader::A_MN_MAJOR ? make_sdesc_sw128_mn(sA, 64 * 128) : make_sdesc_sw128(sA))
+                                   : make_sdesc(sA, TC_BM * 16, 128);
+          const uint64_t bd0 = Loader::B_TMA_SW128
+                                   ? (Loader::B_MN_MAJOR ? make_sdesc_sw128_mn(sB, 64 * 128) : make_sdesc_sw128(sB))
+                                   : make_sdesc(sB, BN * 16, 128);
+          auto issue = [&](int k) {
+            const uint64_t ad = ad0 + (uint64_t)((A_STEP >> 4) * (uint32_t)k);
+            const uint64_t bd = bd0 + (uint64_t)((B_STEP >> 4) * (uint32_t)k);
+            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+            if constexpr (PAIR)
+              umma_bf16_pair_warp(d_tmem, ad, bd, idesc, accum);
+            else
+              umma_bf16_warp(d_tmem, ad, bd, idesc, accum);
+          };
+          if (nk16 == TC_BK / 16) {  // full k-block: one asm block of four MMAs
+            const uint32_t accum = kb > 0 ? 1u : 0u;
+            if constexpr (PAIR)
+              umma4_pair_warp(d_tmem, ad0, bd0, idesc, accum, A_STEP >> 4, B_STEP >> 4);
+            else
+              umma4_warp(d_tmem, ad0, bd0, idesc, accum, A_STEP >> 4, B_STEP >> 4);
+          } else {
+#pragma unroll 1
+            for (int k = 0; k < nk16; ++k) issue(k);
+          }
+          if (lane == 0) TC_TRACE(1, 8, t, kb);
+          if constexpr (PAIR) {
+            umma_commit_pair_warp(&empty[stage]);
+            if (kb == c.nkb - 1) umma_commit_pair_warp(&tfull[acc]);
+          } else {
+            umma_commit_warp(&empty[stage]);
+            if (kb == c.nkb - 1) umma_commit_warp(&tfull[acc]);
+          }
         }
         __syncwarp();
         if (++stage == S) {
@@ -424,13 +522,18 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
         }
       }
     }
+    if (lane == 0) TC_TRACE_DONE(1);
   }
 teardown:
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // rank 0's last MMAs and commits target the peer
   if (warp == R::MMA_WARP) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, L::TMEM_COLS);
+    if constexpr (PAIR)
+      tmem_dealloc_pair(tmem_base, L::TMEM_COLS);
+    else
+      tmem_dealloc(tmem_base, L::TMEM_COLS);
   }
 }
 
@@ -453,6 +556,33 @@ inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& sh
   if (grid < 1) grid = 1;
   kern<<<grid, TcRoles<Loader, Epi>::THREADS, L::TOTAL, st>>>(ld, epi, shape);
   return cudaGetLastError();
+}
+
+// CTA-pair launch: (2,1,1) clusters, one pair per 256-row x BN tile, grid <= the SM count
+template <int BN, class Loader, class Epi>
+inline cudaError_t tc_launch_pair(const Loader& ld, const Epi& epi, const TcShape& shape, int num_sms,
+                                  cudaStream_t st) {
+  using L = TcSmemLayout<BN, TcRoles<Loader, Epi>::EPI_STAGE, 1, BN / 2>;
+  auto kern = tc_gemm_kernel<BN, Loader, Epi, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+  if (e != cudaSuccess) return e;
+  const int tiles = shape.m_tiles * shape.n_tiles * shape.splits;
+  int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  if (pairs < 1) pairs = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs, 1, 1);
+  cfg.blockDim = dim3(TcRoles<Loader, Epi>::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, ld, epi, shape);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace ce

@@ -107,7 +107,8 @@ _lock = threading.Lock()
 
 
 def library_path():
-    return _build.LIB_PATH
+    # CE_LIB=trace: the -DCE_TC_TRACE debug build (tools/tc_trace.py), never the product
+    return _build.TRACE_LIB_PATH if os.environ.get("CE_LIB") == "trace" else _build.LIB_PATH
 
 
 def load(build_if_missing=True):
@@ -117,7 +118,10 @@ def load(build_if_missing=True):
         if _lib is not None:
             return _lib
         path = library_path()
-        if not os.path.exists(path) or (build_if_missing and not _build.up_to_date()):
+        if path == _build.TRACE_LIB_PATH:
+            if not os.path.exists(path):
+                raise OSError(f"{path} missing; run python -m paper_1909_12291_b200.build --trace")
+        elif not os.path.exists(path) or (build_if_missing and not _build.up_to_date()):
             if not build_if_missing:
                 raise OSError(f"{path} missing; run python -m paper_1909_12291_b200.build")
             _build.build()

@@ -42,6 +42,8 @@ def test_tensor_core_kernels_present():
     assert "UTCHMMA" in sass          # tcgen05.mma
     assert "LDTM" in sass             # tcgen05.ld
     assert "LDGSTS" in sass           # cp.async gathers
+    assert "UTCHMMA.2CTA" in sass     # tcgen05.mma.cta_group::2 (CTA-pair conv forward)
+    assert "UTMALDG.4D.IM2COL.2CTA" in sass  # pair im2col TMA completing on the leader's barrier
 
 
 def test_error_path_without_gpu():

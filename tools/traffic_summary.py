@@ -1,6 +1,11 @@
-"""Per-launch DRAM bytes of the dense-backward class from an ncu CSV of the bench's
-profiling pass (tools/gpu/r02_traffic.sh) -> profiles/traffic_r02.json, which
-bench.py reports as roofline.traffic next to the class's algorithmic bytes."""
+"""Per-class DRAM bytes from the ncu CSV of the bench's profiling pass
+(tools/gpu/r02_traffic.sh: kernels renamed after their NVTX class range) ->
+profiles/traffic_r02.json. Each class gets its measured DRAM bytes per class
+bracket (the unit bench.py's events time and roofline.achieved counts), next
+to the bracket count the plain run printed.
+
+    python tools/traffic_summary.py gpurun_out/traffic_all.csv gpurun_out/traffic_plain.log > profiles/traffic_r02.json
+"""
 import collections
 import csv
 import json
@@ -17,19 +22,28 @@ for r in rows:
         continue
     per[r[idi]][r[mi]] = float(r[vi].replace(",", "")) * scale[r[ui]]
     per[r[idi]]["name"] = r[ki]
+counts = {}
+for line in open(sys.argv[2]):
+    if line.startswith("{") and "class_launches" in line:
+        counts = json.loads(line)["class_launches"]
 tot = collections.defaultdict(lambda: [0, 0.0, 0.0])
+kern = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for d in per.values():
-    short = d["name"].split("(")[0].split("<")[0].replace("void ", "").strip()
-    if "tc_gemm_kernel" in d["name"]:
-        short = "tc_" + ("DenseDw" if "DenseDwLoader" in d["name"] else "DenseDx")
-    t = tot[short]
-    t[0] += 1
-    t[1] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
-    t[2] += d.get("gpu__time_duration.sum", 0.0)
-launches = int(sys.argv[2]) if len(sys.argv) > 2 else None  # dense_bwd class launches of the same pass
-total_bytes = sum(v[1] for v in tot.values())
-out = {"source": sys.argv[1], "kernels": {k: {"launches": v[0], "dram_bytes": v[1], "us": v[2]} for k, v in tot.items()},
-       "classes": {"dense_bwd": {"dram_bytes_total": total_bytes,
-                                 "dram_bytes_per_launch": total_bytes / launches if launches else None,
-                                 "class_launches": launches}}}
-print(json.dumps(out, indent=1))
+    cls, _, kname = d["name"].partition("/")  # --print-nvtx-rename kernel: "<class range>/<kernel>"
+    kname = kname.replace("void ", "").split("(")[0].split("<")[0].replace("ce::", "").strip()
+    by = d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    us = d.get("gpu__time_duration.sum", 0.0)
+    for t in (tot[cls], kern[(cls, kname)]):
+        t[0] += 1
+        t[1] += by
+        t[2] += us
+classes = {}
+for name, (kernels, by, us) in sorted(tot.items()):
+    n = counts.get(name)
+    classes[name] = {"kernels": kernels, "dram_bytes_total": by, "us_serial_cold": us, "class_launches": n,
+                     "dram_bytes_per_launch": by / n if n else None,
+                     "by_kernel": {k: {"launches": v[0], "dram_bytes": v[1], "us": v[2]}
+                                   for (c, k), v in sorted(kern.items()) if c == name}}
+print(json.dumps({"source": sys.argv[1], "rule": "ncu dram__bytes_read.sum + dram__bytes_write.sum summed over "
+                  "the kernels inside each class's NVTX range, divided by the class brackets of the same pass",
+                  "classes": classes}, indent=1))
