@@ -67,6 +67,29 @@ inline bool make_tmap_mn64(CUtensorMap* map, const bf16* base, int krows, int mn
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The same [K rows][MN] operand as `nslab` 64-wide MN slabs in ONE copy: a 3-D
+// view {64 MN, K rows, MN / 64 slabs} (slab stride 128 B) whose box lands as
+// nslab consecutive 8 KB SW128 blocks, the layout of nslab make_tmap_mn64 boxes.
+// One TMA issue instead of nslab (the producer's per-copy issue cost dominates
+// short k-blocks: profiles/r02_tc_trace/).
+inline bool make_tmap_mn64_slabs(CUtensorMap* map, const bf16* base, int krows, int mn, int nslab) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+  }
+  if (mn % 64 != 0 || nslab < 1) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)krows, (cuuint64_t)(mn / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)mn * 2, 128};
+  cuuint32_t box[3] = {64, 64, (cuuint32_t)nslab};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)base, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // TMA im2col descriptor over an NHWC bf16 activation for a valid (unpadded)
 // convolution with kernel k and stride s: `pixels` output pixels x 64 channels
 // per copy (128 B rows, SWIZZLE_128B), receptive-field origins traversed in
@@ -253,6 +276,7 @@ struct FwdTcLoader {
   static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2, NARROW = MODE == 3;
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
   static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL || NARROW;
+  static constexpr bool KB2 = IM2COL;  // two k-blocks per pipeline stage (tc_engine)
   CUtensorMap wmap;  // B operand (weights) when TMA_B
   CUtensorMap xmap;  // im2col view of x when IM2COL
   const bf16* x;
@@ -398,7 +422,7 @@ struct FwdBlockLoader {
 // rank 0 primes with the pair's total bytes.
 struct FwdTcLoaderPair {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true;
+  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true, KB2 = true;
   CUtensorMap wmap;  // box: 64 K x BN / 2 rows
   CUtensorMap xmap;  // im2col, 128 pixels x 64 channels
   ConvGeom g;
@@ -589,6 +613,7 @@ struct DgradTcLoader {
   static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2, NARROW = MODE == 3;
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
   static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL || NARROW;
+  static constexpr bool KB2 = IM2COL;
   CUtensorMap wmap;  // class block [c][K] when TMA_B
   CUtensorMap dmap;  // im2col view of dY for this class when IM2COL
   const bf16* dy;
@@ -729,7 +754,7 @@ inline bool make_tmap_im2col_dgrad(CUtensorMap* map, const bf16* dy, const ConvG
 // class's im2col view of dY and its weight block
 struct DgradTcLoaderPair {
   static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
-  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true;
+  static constexpr bool A_TMA_SW128 = true, B_TMA_SW128 = true, PURE_TMA = true, KB2 = true;
   CUtensorMap wmap;  // class block [c][K], box 64 K x BN / 2 rows
   CUtensorMap dmap;
   ConvGeom g;
@@ -792,7 +817,10 @@ struct WgradTcLoader {
   static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2;
   static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
   static constexpr bool A_TMA_SW128 = IM2COL, B_TMA_SW128 = TMA_B, PURE_TMA = IM2COL;
+  static constexpr bool KB2 = IM2COL;
   CUtensorMap dmap;  // dY [Mo][co] as 64x64 MN-major SW128 boxes when TMA_B
+  CUtensorMap dmap3;  // dY as BN/64 slabs in one copy (make_tmap_mn64_slabs) when slab3
+  int slab3;
   CUtensorMap xmap;  // im2col view of x (64 pixels x 64 channels) when IM2COL
   const bf16* x;
   const bf16* dy;
@@ -821,7 +849,10 @@ struct WgradTcLoader {
         tma_load_im2col_4d(sA + blk * 8192, &xmap, c0, (int)q * g.s, (int)p * g.s, (int)n, (uint16_t)j,
                            (uint16_t)i, full);
       }
-      for (int jb = 0; jb < BN / 64; ++jb) tma_load_2d(sB + jb * 8192, &dmap, c.n0 + 64 * jb, kb * TC_BK, full);
+      if (slab3)
+        tma_load_3d(sB, &dmap3, 0, kb * TC_BK, c.n0 / 64, full);
+      else
+        for (int jb = 0; jb < BN / 64; ++jb) tma_load_2d(sB + jb * 8192, &dmap, c.n0 + 64 * jb, kb * TC_BK, full);
       return;
     }
     // A: 16 groups of 8 (i,j,c) rows x 64 reduction indices; 256 producers -> 4 chunks each
@@ -1424,6 +1455,7 @@ inline int conv_wgrad_tc(const ConvGeom& g, const bf16* x, const bf16* dy, float
     if (tma && g.c % 64 == 0 && !im2col_disabled() && make_tmap_mn64(&ld2.dmap, dy, Mo, g.co) &&
         make_tmap_im2col(&ld2.xmap, x, g, TC_BK)) {
       fill(ld2);
+      ld2.slab3 = BN > 64 && make_tmap_mn64_slabs(&ld2.dmap3, dy, Mo, g.co, BN / 64) ? 1 : 0;
       e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
     } else if (tma && make_tmap_mn64(&ld1.dmap, dy, Mo, g.co)) {
       fill(ld1);

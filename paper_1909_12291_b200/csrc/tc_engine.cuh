@@ -106,6 +106,15 @@ struct Split3 : std::false_type {};
 template <class Loader>
 struct Split3<Loader, std::void_t<decltype(Loader::SPLIT3)>> : std::bool_constant<Loader::SPLIT3> {};
 
+// Loader::KB2: a pipeline stage holds TWO consecutive 64-deep k-blocks (pure-TMA
+// loaders): one barrier round trip, arrive and commit per 128 of K. The trace
+// (profiles/r02_tc_trace/) shows ~650-700 SM cycles of fixed producer / MMA-warp
+// cost per stage, more than a 128 x 128 x 64 block's 256 cycles of MMA work.
+template <class Loader, class = void>
+struct Kb2 : std::false_type {};
+template <class Loader>
+struct Kb2<Loader, std::void_t<decltype(Loader::KB2)>> : std::bool_constant<Loader::KB2> {};
+
 template <class Loader, class Epi>
 struct TcRoles {
   static constexpr int PW = ProducerWarps<Loader>::value;
@@ -194,8 +203,9 @@ __device__ inline TileCoord tc_tile(const TcShape& s, int t, int bn) {
   return c;
 }
 
-// BROWS: B rows held per CTA (BN, or BN / 2 for a CTA pair)
-template <int BN, int EPI_STAGE = 0, int PLANES = 1, int BROWS = BN>
+// BROWS: B rows held per CTA (BN, or BN / 2 for a CTA pair). TABLE: loader table
+// bytes (pure-TMA loaders use none, which leaves that space to the ring).
+template <int BN, int EPI_STAGE = 0, int PLANES = 1, int BROWS = BN, int TABLE = TC_TABLE_BYTES>
 struct TcSmemLayout {
   static constexpr int A_PLANE = TC_BM * TC_BK * 2;  // 16 KB
   static constexpr int B_PLANE = BROWS * TC_BK * 2;
@@ -203,7 +213,7 @@ struct TcSmemLayout {
   static constexpr int B_BYTES = B_PLANE * PLANES;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // pipeline budget: 196 KB less any epilogue staging beyond the 8 KB of 8 staged warps
-  static constexpr int RING = 196 * 1024 - (EPI_STAGE > 8192 ? EPI_STAGE - 8192 : 0);
+  static constexpr int RING = 196 * 1024 + (TC_TABLE_BYTES - TABLE) - (EPI_STAGE > 8192 ? EPI_STAGE - 8192 : 0);
   static constexpr int STAGES = (RING / STAGE_BYTES) > 8 ? 8 : (RING / STAGE_BYTES);
   static constexpr int LAG = STAGES - 1 > TC_MAX_LAG ? TC_MAX_LAG : STAGES - 1;  // cp.async groups in flight
   // SPLIT3 keeps two accumulators per buffer (hi*hi and the cross terms)
@@ -211,7 +221,19 @@ struct TcSmemLayout {
   static constexpr int TMEM_COLS = (2 * ACC_COLS <= 32) ? 32 : (2 * ACC_COLS <= 64) ? 64 : (2 * ACC_COLS <= 128) ? 128
                                    : (2 * ACC_COLS <= 256) ? 256 : 512;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
-  static constexpr int TOTAL = STAGES * STAGE_BYTES + TC_TABLE_BYTES + BAR_BYTES + EPI_STAGE + 1024;  // + slack
+  static constexpr int TABLE_BYTES = TABLE;
+  static constexpr int TOTAL = STAGES * STAGE_BYTES + TABLE + BAR_BYTES + EPI_STAGE + 1024;  // + slack
+};
+
+// Shared-memory layout of one (BN, Loader, Epi, PAIR) kernel: KB2 stages (two
+// k-blocks) where the ring still holds >= 3 of them, i.e. <= 128 B rows per CTA
+template <int BN, class Loader, class Epi, bool PAIR>
+struct TcKernelLayout {
+  static constexpr bool SPLIT = Split3<Loader>::value;
+  static constexpr int BROWS = PAIR ? BN / 2 : BN;
+  static constexpr bool KB2 = Kb2<Loader>::value && !SPLIT && Loader::PURE_TMA && BROWS <= 128;
+  using type = TcSmemLayout<BN, TcRoles<Loader, Epi>::EPI_STAGE, SPLIT ? 3 : (KB2 ? 2 : 1), BROWS,
+                            Loader::PURE_TMA ? 0 : TC_TABLE_BYTES>;
 };
 
 // PAIR: the CTA-pair variant (cta_group::2, launched as (2,1,1) clusters). A
@@ -228,17 +250,19 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
   constexpr int WSM = EpiWarpSmem<Epi>::value;
   constexpr bool SPLIT = Split3<Loader>::value;
   static_assert(!PAIR || (Loader::PURE_TMA && !SPLIT && BN >= 32), "CTA pairs: pure-TMA loaders, BN >= 32");
-  using L = TcSmemLayout<BN, R::EPI_STAGE, SPLIT ? 3 : 1, PAIR ? BN / 2 : BN>;
+  using L = typename TcKernelLayout<BN, Loader, Epi, PAIR>::type;
+  constexpr bool KB2 = TcKernelLayout<BN, Loader, Epi, PAIR>::KB2;
+  constexpr int KPS = KB2 ? 2 : 1;  // k-blocks per stage (planes of the stage)
   constexpr int S = L::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* table = smem + S * L::STAGE_BYTES;
-  uint64_t* full = (uint64_t*)(table + TC_TABLE_BYTES);
+  uint64_t* full = (uint64_t*)(table + L::TABLE_BYTES);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base_slot = (uint32_t*)(tempty + 2);
-  uint8_t* epi_stage = table + TC_TABLE_BYTES + L::BAR_BYTES;  // epilogue warp staging / scratch (16-B aligned)
+  uint8_t* epi_stage = table + L::TABLE_BYTES + L::BAR_BYTES;  // epilogue warp staging / scratch (16-B aligned)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -291,7 +315,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     int npending = 0;
     for (int t = tile0; t < total_tiles; t += tstep) {
       TileCoord c = tile_at(t);
-      for (int kb = 0; kb < c.nkb; ++kb) {
+      for (int kb = 0; kb < c.nkb; kb += KPS) {
         if (threadIdx.x == 0) TC_TRACE(0, 1, t, kb);
         mbar_wait(&empty[stage], phase ^ 1);
         if (threadIdx.x == 0) TC_TRACE(0, 2, t, kb);
@@ -301,7 +325,11 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
 #ifdef CE_TC_TRACE
           if (!g_tc_fake_load)
 #endif
-          ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
+          {
+            ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
+            if (KB2 && kb + 1 < c.nkb)  // second k-block into the stage's second planes
+              ld.load(c, c.kb0 + kb + 1, sA + L::A_PLANE, sB + L::B_PLANE, ptid, table, &full[stage]);
+          }
           TC_TRACE(0, 7, t, kb);
           if (!PAIR || rank == 0) mbar_arrive(&full[stage]);
         } else if constexpr (SyncFill<Loader>::value) {  // st.shared fill: visible to the MMA after the fence
@@ -444,7 +472,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * L::ACC_COLS);
       if (lane == 0) TC_TRACE(1, 4, t, 0);
-      for (int kb = 0; kb < c.nkb; ++kb) {
+      for (int kb = 0; kb < c.nkb; kb += KPS) {
         mbar_wait_warp(&full[stage], phase);
         if (lane == 0) TC_TRACE(1, 3, t, kb);
         tc_fence_after();
@@ -453,6 +481,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
         const int gkb = c.kb0 + kb;
         int nk16 = k16_total - gkb * (TC_BK / 16);
         if (nk16 > TC_BK / 16) nk16 = TC_BK / 16;
+        const bool last_stage = kb + KPS >= c.nkb;
         if constexpr (SPLIT) {
           if (lane == 0) {
 #pragma unroll 1
@@ -481,38 +510,47 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
           // no-swizzle K-major: +2 chunk columns (2 x rows x 16 B). Descriptor address field = bytes >> 4.
           constexpr uint32_t A_STEP = Loader::A_TMA_SW128 ? (Loader::A_MN_MAJOR ? 2048u : 32u) : 2u * TC_BM * 16u;
           constexpr uint32_t B_STEP = Loader::B_TMA_SW128 ? (Loader::B_MN_MAJOR ? 2048u : 32u) : 2u * BN * 16u;
-          const uint64_t ad0 = Loader::A_TMA_SW128
-                                   ? (Loader::A_MN_MAJOR ? make_sdesc_sw128_mn(sA, 64 * 128) : make_sdesc_sw128(sA))
-                                   : make_sdesc(sA, TC_BM * 16, 128);
-          const uint64_t bd0 = Loader::B_TMA_SW128
-                                   ? (Loader::B_MN_MAJOR ? make_sdesc_sw128_mn(sB, 64 * 128) : make_sdesc_sw128(sB))
-                                   : make_sdesc(sB, BN * 16, 128);
-          auto issue = [&](int k) {
-            const uint64_t ad = ad0 + (uint64_t)((A_STEP >> 4) * (uint32_t)k);
-            const uint64_t bd = bd0 + (uint64_t)((B_STEP >> 4) * (uint32_t)k);
-            const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-            if constexpr (PAIR)
-              umma_bf16_pair_warp(d_tmem, ad, bd, idesc, accum);
-            else
-              umma_bf16_warp(d_tmem, ad, bd, idesc, accum);
-          };
-          if (nk16 == TC_BK / 16) {  // full k-block: one asm block of four MMAs
-            const uint32_t accum = kb > 0 ? 1u : 0u;
-            if constexpr (PAIR)
-              umma4_pair_warp(d_tmem, ad0, bd0, idesc, accum, A_STEP >> 4, B_STEP >> 4);
-            else
-              umma4_warp(d_tmem, ad0, bd0, idesc, accum, A_STEP >> 4, B_STEP >> 4);
-          } else {
+          // one 64-deep k-block (planes h of the stage): MMAs over its nk K=16 steps
+          auto kblock = [&](int h, int kbi, int nk) {
+            const uint32_t pA = sA + (uint32_t)h * L::A_PLANE, pB = sB + (uint32_t)h * L::B_PLANE;
+            const uint64_t ad0 = Loader::A_TMA_SW128
+                                     ? (Loader::A_MN_MAJOR ? make_sdesc_sw128_mn(pA, 64 * 128) : make_sdesc_sw128(pA))
+                                     : make_sdesc(pA, TC_BM * 16, 128);
+            const uint64_t bd0 = Loader::B_TMA_SW128
+                                     ? (Loader::B_MN_MAJOR ? make_sdesc_sw128_mn(pB, 64 * 128) : make_sdesc_sw128(pB))
+                                     : make_sdesc(pB, BN * 16, 128);
+            if (nk == TC_BK / 16) {  // full k-block: one asm block of four MMAs
+              const uint32_t accum = kbi > 0 ? 1u : 0u;
+              if constexpr (PAIR)
+                umma4_pair_warp(d_tmem, ad0, bd0, idesc, accum, A_STEP >> 4, B_STEP >> 4);
+              else
+                umma4_warp(d_tmem, ad0, bd0, idesc, accum, A_STEP >> 4, B_STEP >> 4);
+            } else {
 #pragma unroll 1
-            for (int k = 0; k < nk16; ++k) issue(k);
+              for (int k = 0; k < nk; ++k) {
+                const uint64_t ad = ad0 + (uint64_t)((A_STEP >> 4) * (uint32_t)k);
+                const uint64_t bd = bd0 + (uint64_t)((B_STEP >> 4) * (uint32_t)k);
+                const uint32_t accum = (kbi > 0 || k > 0) ? 1u : 0u;
+                if constexpr (PAIR)
+                  umma_bf16_pair_warp(d_tmem, ad, bd, idesc, accum);
+                else
+                  umma_bf16_warp(d_tmem, ad, bd, idesc, accum);
+              }
+            }
+          };
+          kblock(0, kb, nk16);
+          if (KB2 && kb + 1 < c.nkb) {
+            int nk2 = k16_total - (gkb + 1) * (TC_BK / 16);
+            if (nk2 > TC_BK / 16) nk2 = TC_BK / 16;
+            kblock(1, kb + 1, nk2);
           }
           if (lane == 0) TC_TRACE(1, 8, t, kb);
           if constexpr (PAIR) {
             umma_commit_pair_warp(&empty[stage]);
-            if (kb == c.nkb - 1) umma_commit_pair_warp(&tfull[acc]);
+            if (last_stage) umma_commit_pair_warp(&tfull[acc]);
           } else {
             umma_commit_warp(&empty[stage]);
-            if (kb == c.nkb - 1) umma_commit_warp(&tfull[acc]);
+            if (last_stage) umma_commit_warp(&tfull[acc]);
           }
         }
         __syncwarp();
@@ -547,7 +585,7 @@ __device__ __forceinline__ uint32_t mnmajor_off(int R, int g, int kk) {
 
 template <int BN, class Loader, class Epi>
 inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& shape, int num_sms, cudaStream_t st) {
-  using L = TcSmemLayout<BN, TcRoles<Loader, Epi>::EPI_STAGE, Split3<Loader>::value ? 3 : 1>;
+  using L = typename TcKernelLayout<BN, Loader, Epi, false>::type;
   auto kern = tc_gemm_kernel<BN, Loader, Epi>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
   if (e != cudaSuccess) return e;
@@ -562,7 +600,7 @@ inline cudaError_t tc_launch(const Loader& ld, const Epi& epi, const TcShape& sh
 template <int BN, class Loader, class Epi>
 inline cudaError_t tc_launch_pair(const Loader& ld, const Epi& epi, const TcShape& shape, int num_sms,
                                   cudaStream_t st) {
-  using L = TcSmemLayout<BN, TcRoles<Loader, Epi>::EPI_STAGE, 1, BN / 2>;
+  using L = typename TcKernelLayout<BN, Loader, Epi, true>::type;
   auto kern = tc_gemm_kernel<BN, Loader, Epi, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
   if (e != cudaSuccess) return e;
