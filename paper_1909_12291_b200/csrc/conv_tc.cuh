@@ -285,6 +285,7 @@ struct FwdTcLoader {
   int K, M, BN;
   FastDiv d_ow, d_oh;
   PoolMap pm;  // POOL
+  FastDiv d_cpb, d_k;  // k-block -> (tap, 64-channel slab), tap -> (i, j) (IM2COL)
   static_assert(!POOL || MODE <= 1, "the pooled row order needs the gather loader");
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
     if ((IM2COL || NARROW) && tid == 0) {
@@ -303,9 +304,10 @@ struct FwdTcLoader {
                        uint64_t* full) const {
     const int* xoff = (const int*)table;
     if (IM2COL) {  // one thread: A via im2col TMA (tap, 64-channel slab), B via 2-D TMA
-      const int cpb = g.c / 64;
-      const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
-      const int i = tap / g.k, j = tap - i * g.k;
+      uint32_t tap, slab, i, j;  // FastDiv: runtime integer divisions cost ~100 cycles each here
+      d_cpb.divmod((uint32_t)kb, tap, slab);
+      d_k.divmod(tap, i, j);
+      const int c0 = (int)slab * 64;
       uint32_t q, p, n, t;
       d_ow.divmod((uint32_t)c.m0, t, q);
       d_oh.divmod(t, n, p);
@@ -390,6 +392,7 @@ struct FwdBlockLoader {
   CUtensorMap xmap;  // make_tmap_blocks
   PixelBlocks pb;
   int cin, k, BN;
+  FastDiv d_cpb, d_k;
   __device__ void init(uint8_t*, int tid, int) const {
     if (tid == 0) {
       tma_prefetch_desc(&wmap);
@@ -398,9 +401,10 @@ struct FwdBlockLoader {
   }
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
                        uint64_t* full) const {
-    const int cpb = cin / 64;
-    const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
-    const int i = tap / k, j = tap - i * k;
+    uint32_t tap, slab, i, j;
+    d_cpb.divmod((uint32_t)kb, tap, slab);
+    d_k.divmod(tap, i, j);
+    const int c0 = (int)slab * 64;
     int img, p0, q0;
     pb.origin(c.m0, img, p0, q0);
     if constexpr (PAIR) {
@@ -427,14 +431,15 @@ struct FwdTcLoaderPair {
   CUtensorMap xmap;  // im2col, 128 pixels x 64 channels
   ConvGeom g;
   int K, M, BN;
-  FastDiv d_ow, d_oh;
+  FastDiv d_ow, d_oh, d_cpb, d_k;
   __device__ void init(uint8_t*, int, int) const {}
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
                        uint64_t* full) const {
     const uint32_t rank = cluster_ctarank();
-    const int cpb = g.c / 64;
-    const int tap = kb / cpb, c0 = (kb - tap * cpb) * 64;
-    const int i = tap / g.k, j = tap - i * g.k;
+    uint32_t tap, slab, i, j;
+    d_cpb.divmod((uint32_t)kb, tap, slab);
+    d_k.divmod(tap, i, j);
+    const int c0 = (int)slab * 64;
     uint32_t q, p, n, t;
     d_ow.divmod((uint32_t)c.m0, t, q);
     d_oh.divmod(t, n, p);
@@ -621,7 +626,7 @@ struct DgradTcLoader {
   ConvGeom g;
   DgradClass cl;
   int K, M, BN;    // K = ti*tj*co, M = n*hc*wc
-  FastDiv d_wc, d_hc;
+  FastDiv d_wc, d_hc, d_cpb, d_tj;
   __device__ void init(uint8_t* table, int tid, int nthreads) const {
     if (IM2COL || NARROW) return;
     const int nk8 = K / 8;
@@ -643,9 +648,10 @@ struct DgradTcLoader {
                        uint64_t* full) const {
     const int nk8 = K / 8;
     if (IM2COL) {  // one thread: A = im2col of dY (flipped class taps, 64 channels), B = class weights
-      const int cpb = g.co / 64;
-      const int tap = kb / cpb, o0 = (kb - tap * cpb) * 64;
-      const int ap = tap / cl.tj, bp = tap - ap * cl.tj;
+      uint32_t tap, slab, ap, bp;
+      d_cpb.divmod((uint32_t)kb, tap, slab);
+      d_tj.divmod(tap, ap, bp);
+      const int o0 = (int)slab * 64;
       uint32_t ww, hh, n, t;
       d_wc.divmod((uint32_t)c.m0, t, ww);
       d_hc.divmod(t, n, hh);
@@ -760,14 +766,15 @@ struct DgradTcLoaderPair {
   ConvGeom g;
   DgradClass cl;
   int K, M, BN;
-  FastDiv d_wc, d_hc;
+  FastDiv d_wc, d_hc, d_cpb, d_tj;
   __device__ void init(uint8_t*, int, int) const {}
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
                        uint64_t* full) const {
     const uint32_t rank = cluster_ctarank();
-    const int cpb = g.co / 64;
-    const int tap = kb / cpb, o0 = (kb - tap * cpb) * 64;
-    const int ap = tap / cl.tj, bp = tap - ap * cl.tj;
+    uint32_t tap, slab, ap, bp;
+    d_cpb.divmod((uint32_t)kb, tap, slab);
+    d_tj.divmod(tap, ap, bp);
+    const int o0 = (int)slab * 64;
     uint32_t ww, hh, n, t;
     d_wc.divmod((uint32_t)c.m0, t, ww);
     d_hc.divmod(t, n, hh);
@@ -828,7 +835,7 @@ struct WgradTcLoader {
   int Kf;  // k*k*c (rows of D)
   int Mo;  // reduction length n*oh*ow
   int BN;
-  FastDiv d_ow, d_oh;
+  FastDiv d_ow, d_oh, d_c, d_k;
   __device__ void init(uint8_t*, int, int) const {}
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t*,
                        uint64_t* full) const {
@@ -843,9 +850,9 @@ struct WgradTcLoader {
       bytes += (uint32_t)nblk * 64u * TC_BK * 2u;
       mbar_expect_tx(full, bytes);
       for (int blk = 0; blk < nblk; ++blk) {
-        const int kk0 = c.m0 + 64 * blk;
-        const int tap = kk0 / g.c, c0 = kk0 - tap * g.c;
-        const int i = tap / g.k, j = tap - i * g.k;
+        uint32_t tap, c0, i, j;
+        d_c.divmod((uint32_t)(c.m0 + 64 * blk), tap, c0);
+        d_k.divmod(tap, i, j);
         tma_load_im2col_4d(sA + blk * 8192, &xmap, c0, (int)q * g.s, (int)p * g.s, (int)n, (uint16_t)j,
                            (uint16_t)i, full);
       }
@@ -1051,6 +1058,7 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
     auto fill = [&](auto& ld) {
       ld.x = x; ld.w = w; ld.g = g; ld.K = K; ld.M = M; ld.BN = BN;
       ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      ld.d_cpb = FastDiv((uint32_t)std::max(1, g.c / 64)); ld.d_k = FastDiv(g.k);
     };
     FwdTcLoader<2> ld2{};
     FwdTcLoader<3> ld3{};
@@ -1095,6 +1103,7 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
           !make_tmap_blocks(&ld.xmap, x, g.n, g.h, g.w, g.c, pbk.bh, 1 << pbk.bw_log2))
         return -1;
       ld.pb = pbk; ld.cin = g.c; ld.k = g.k; ld.BN = BN;
+      ld.d_cpb = FastDiv(g.c / 64); ld.d_k = FastDiv(g.k);
       FwdTcEpi ep{y, bias, M, g.co, relu};
       ep.pb = pbk;
       TcShape sh = tc_make_shape(tiles * TC_BM, g.co, K, BN, 1);
@@ -1125,6 +1134,7 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
       if (!make_tmap_kmajor(&ld.wmap, w, g.co, K, BN / 2) || !make_tmap_im2col(&ld.xmap, x, g, TC_BM)) return -1;
       ld.g = g; ld.K = K; ld.M = M; ld.BN = BN;
       ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      ld.d_cpb = FastDiv(g.c / 64); ld.d_k = FastDiv(g.k);
       TcShape sh = tc_make_shape(M, g.co, K, BN, 1);
       sh.m_tiles = (M + 2 * TC_BM - 1) / (2 * TC_BM);
       cudaError_t e = tc_launch_pair<BN>(ld, FwdTcEpi{y, bias, M, g.co, relu}, sh, num_sms, st);
@@ -1349,6 +1359,7 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
             return -1;
           ld.g = g; ld.cl = cl; ld.K = K; ld.M = M; ld.BN = BN;
           ld.d_wc = FastDiv(cl.wc); ld.d_hc = FastDiv(cl.hc);
+          ld.d_cpb = FastDiv(g.co / 64); ld.d_tj = FastDiv(cl.tj);
           TcShape sh = tc_make_shape(M, g.c, K, BN, 1);
           sh.m_tiles = (M + 2 * TC_BM - 1) / (2 * TC_BM);
           DgradTcEpi ep{dx, mask, g, cl, M, FastDiv(cl.wc), FastDiv(cl.hc)};
@@ -1370,6 +1381,7 @@ inline int conv_dgrad_tc(const ConvGeom& g, const bf16* dy, const bf16* wt, cons
         auto fill = [&](auto& ld) {
           ld.dy = dy; ld.wt = wcls; ld.g = g; ld.cl = cl; ld.K = K; ld.M = M; ld.BN = BN;
           ld.d_wc = FastDiv(cl.wc); ld.d_hc = FastDiv(cl.hc);
+          ld.d_cpb = FastDiv((uint32_t)std::max(1, g.co / 64)); ld.d_tj = FastDiv(cl.tj);
         };
         DgradTcLoader<2> ld2{};
         DgradTcLoader<3> ld3{};
@@ -1449,6 +1461,7 @@ inline int conv_wgrad_tc(const ConvGeom& g, const bf16* x, const bf16* dy, float
     auto fill = [&](auto& ld) {
       ld.x = x; ld.dy = dy; ld.g = g; ld.Kf = Kf; ld.Mo = Mo; ld.BN = BN;
       ld.d_ow = FastDiv(g.ow); ld.d_oh = FastDiv(g.oh);
+      ld.d_c = FastDiv(g.c); ld.d_k = FastDiv(g.k);
     };
     WgradTcLoader<2> ld2{};
     WgradTcLoader<1> ld1{};

@@ -9,5 +9,5 @@ timeout 300 python tools/conv_bench.py vgg 64,256,97,256,4,1 > gpurun_out/wg_ben
 export CE_LIB=trace
 : > gpurun_out/trace7.jsonl
 for sh in 64,128,46,128,3,1 64,256,97,256,4,1 64,256,20,256,3,1; do
-  timeout 120 python tools/tc_trace.py $sh wgrad >> gpurun_out/trace7.jsonl 2>>gpurun_out/trace7.err
+  for p in fwd dgrad wgrad; do CE_CONV_PAIR=0 timeout 120 python tools/tc_trace.py $sh $p >> gpurun_out/trace7.jsonl 2>>gpurun_out/trace7.err; done
 done
