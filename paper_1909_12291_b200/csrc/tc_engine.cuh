@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
           mbar_arrive(&full[stage]);
         } else {
           ld.load(c, c.kb0 + kb, sA, sB, ptid, table, &full[stage]);
+          if (threadIdx.x == 0) TC_TRACE(0, 7, t, kb);
           cp_async_commit();
           // retire the oldest group once LAG newer ones are in flight
           if (npending == LAG) {

@@ -63,8 +63,17 @@ def main():
     ws = torch.empty(native.conv_workspace_bytes(desc), dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
 
+    pool = next((tuple(int(v) for v in a.split("=")[1].split(",")) for a in args if a.startswith("pool=")), None)
+    if pool:
+        ph = (oh - pool[0]) // pool[1] + 1
+        yp = torch.empty(n, ph, ph, co, device="cuda", dtype=torch.bfloat16)
+        ap = torch.empty(n, ph, ph, co, device="cuda", dtype=torch.uint8)
+
     def run():
-        if p == "fwd":
+        if p == "fwd" and pool:
+            native.conv_fwd(desc, x.data_ptr(), w.data_ptr(), b.data_ptr(), 1, yp.data_ptr(), st, pool=pool,
+                            arg=ap.data_ptr())
+        elif p == "fwd":
             native.conv_fwd(desc, x.data_ptr(), w.data_ptr(), b.data_ptr(), 1, y.data_ptr(), st)
         elif p == "dgrad":
             native.conv_dgrad(desc, dy.data_ptr(), w.data_ptr(), 0, dx.data_ptr(), ws.data_ptr(), ws.numel(), st)
