@@ -109,7 +109,9 @@ inline bool make_tmap_im2col(CUtensorMap* map, const bf16* x, const ConvGeom& g,
   cuuint32_t estr[4] = {1, (cuuint32_t)g.s, (cuuint32_t)g.s, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)x, dims, strides, lower, upper,
                       (cuuint32_t)cpp, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      cpp == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                      cpp == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                      : cpp == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
   // driver <= 13.1 workaround (as in CUTLASS): small tensors must not set bit 21 of word 1
@@ -269,6 +271,60 @@ inline bool pool_fusable(int ps, int pst) { return (ps == 2 || ps == 3) && pst >
 // output pixel's receptive-field origin: (i*W + j)*C + c0.
 // POOL: rows in the window-major order of `pm` (gather modes 0 / 1 only).
 template <int MODE, bool POOL = false>
+struct FwdTcLoader;
+
+// 32-channel im2col forward (C % 64 == 32, e.g. the FIXED genome's second layer):
+// per k-block two TMA im2col boxes of 128 pixels x 32 channels (SWIZZLE_64B, one per
+// 32-deep K half: tap 2kb and 2kb+1 when C = 32) + the weight box. Replaces the
+// cp.async gather, whose 1,024 16-byte requests per k-block cost ~2,200 SM cycles
+// (profiles/r02_tc_trace/).
+struct FwdTcLoader32 {
+  static constexpr int A_MN_MAJOR = 0, B_MN_MAJOR = 0;
+  static constexpr bool A_TMA_SW128 = false, A_SW64 = true, B_TMA_SW128 = true, PURE_TMA = true, KB2 = true;
+  CUtensorMap wmap, xmap;
+  ConvGeom g;
+  int K, M, BN;
+  FastDiv d_ow, d_oh, d_c, d_k;
+  __device__ void init(uint8_t*, int tid, int) const {
+    if (tid == 0) {
+      tma_prefetch_desc(&wmap);
+      tma_prefetch_desc(&xmap);
+    }
+  }
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
+                       uint64_t* full) const {
+    uint32_t q, p, n, t;
+    d_ow.divmod((uint32_t)c.m0, t, q);
+    d_oh.divmod(t, n, p);
+    mbar_expect_tx(full, (uint32_t)(2 * TC_BM * 64 + BN * 128));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t kk = (uint32_t)(kb * TC_BK + h * 32);
+      uint32_t tap = 0, c0 = (uint32_t)g.c, i = 0, j = 0;  // past K: a fully out-of-bounds box zero-fills
+      if ((int)kk < K) {
+        d_c.divmod(kk, tap, c0);
+        d_k.divmod(tap, i, j);
+      }
+      tma_load_im2col_4d(sA + (uint32_t)h * (TC_BM * 64), &xmap, (int)c0, (int)q * g.s, (int)p * g.s, (int)n,
+                         (uint16_t)j, (uint16_t)i, full);
+    }
+    tma_load_2d(sB, &wmap, kb * TC_BK, c.n0, full);
+  }
+};
+
+// 32-channel TMA path enabled (CE_IM2COL32=0: the cp.async gather, for comparison)
+inline bool im2col32_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CE_IM2COL32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline bool im2col32_ok(const ConvGeom& g) {
+  return im2col32_enabled() && g.c % 32 == 0 && g.c % 64 != 0 && !tma_disabled() && !im2col_disabled();
+}
+
+template <int MODE, bool POOL>
 struct FwdTcLoader {
   // MODE 0: cp.async gather A + cp.async B; 1: gather A + TMA B;
   //      2: TMA im2col A (64-channel slabs, SW128) + TMA B;
@@ -1067,6 +1123,14 @@ inline int conv_fwd_tc(const ConvGeom& g, const bf16* x, const bf16* w, const fl
         make_tmap_im2col(&ld2.xmap, x, g, TC_BM)) {
       fill(ld2);
       return tc_launch<BN>(ld2, ep, sh, num_sms, st);
+    }
+    if (tma && im2col32_ok(g)) {
+      FwdTcLoader32 ld32{};
+      if (make_tmap_kmajor(&ld32.wmap, w, g.co, K, BN) && make_tmap_im2col(&ld32.xmap, x, g, TC_BM, 32)) {
+        ld32.g = g; ld32.K = K; ld32.M = M; ld32.BN = BN;
+        ld32.d_ow = FastDiv(g.ow); ld32.d_oh = FastDiv(g.oh); ld32.d_c = FastDiv(g.c); ld32.d_k = FastDiv(g.k);
+        return tc_launch<BN>(ld32, ep, sh, num_sms, st);
+      }
     }
     if (tma && narrow_im2col_enabled() && make_tmap_kmajor(&ld3.wmap, w, g.co, K, BN) &&
         make_tmap_im2col(&ld3.xmap, x, g, TC_BM, 8)) {

@@ -1056,7 +1056,7 @@ int ce_net_create(const ce_net_desc* d, int device, int precision, ce_net** out)
                packed_kp(l.g, l.c_real) <= kPackedMaxKp && Mo * packed_kp(l.g, l.c_real) / 8 < (1ll << 32);
     if (i + 1 < net->L.size() && net->L[i + 1].kind == CE_LAYER_POOL && net->use_tc &&
         pool_fusable(net->L[i + 1].g.k, net->L[i + 1].g.s) && pool_fusion_mode() > 0 &&
-        (pool_fusion_mode() >= 2 || l.packed || l.g.c % 64 != 0)) {
+        (pool_fusion_mode() >= 2 || l.packed || (l.g.c % 64 != 0 && !im2col32_ok(l.g)))) {
       l.pool_fused = true;
       net->L[i + 1].fused = true;
     }

@@ -343,6 +343,19 @@ CE_DEV uint64_t make_sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
+// K-major SWIZZLE_64B canonical layout (a TMA box of 32 bf16 x rows with
+// CU_TENSOR_MAP_SWIZZLE_64B): rows 64 B apart, 8-row atoms of 512 B (SBO); a
+// 64-deep k-block is two such 32-wide regions, a K=16 step advances 32 B inside one.
+CE_DEV uint64_t make_sdesc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;   // SBO = 8 rows x 64 B
+  d |= (uint64_t)1 << 46;            // version
+  d |= (uint64_t)4 << 61;            // SWIZZLE_64B
+  return d;
+}
+
 // MN-major SWIZZLE_128B canonical layout (TMA box of 64 MN-elements x 64 K-rows):
 // K rows 128 B apart, 8-row K groups 1024 B apart (SBO), 64-wide MN blocks LBO
 // apart; one 16-deep MMA K step advances the start address by 2 K groups.

@@ -115,6 +115,13 @@ struct Kb2 : std::false_type {};
 template <class Loader>
 struct Kb2<Loader, std::void_t<decltype(Loader::KB2)>> : std::bool_constant<Loader::KB2> {};
 
+// Loader::A_SW64: A arrives as two 32-wide K-major SWIZZLE_64B regions per k-block
+// (128 rows x 64 B each, 8 KB apart): 32-channel im2col boxes (C % 64 == 32)
+template <class Loader, class = void>
+struct ASw64 : std::false_type {};
+template <class Loader>
+struct ASw64<Loader, std::void_t<decltype(Loader::A_SW64)>> : std::bool_constant<Loader::A_SW64> {};
+
 template <class Loader, class Epi>
 struct TcRoles {
   static constexpr int PW = ProducerWarps<Loader>::value;
@@ -520,7 +527,19 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
             const uint64_t bd0 = Loader::B_TMA_SW128
                                      ? (Loader::B_MN_MAJOR ? make_sdesc_sw128_mn(pB, 64 * 128) : make_sdesc_sw128(pB))
                                      : make_sdesc(pB, BN * 16, 128);
-            if (nk == TC_BK / 16) {  // full k-block: one asm block of four MMAs
+            if constexpr (ASw64<Loader>::value) {  // A: region k/2 (8 KB apart), +32 B for odd k
+#pragma unroll 1
+              for (int k = 0; k < nk; ++k) {
+                const uint64_t ad = make_sdesc_sw64(pA + (uint32_t)(k >> 1) * (TC_BM * 64) + (uint32_t)(k & 1) * 32);
+                const uint64_t bd = bd0 + (uint64_t)((B_STEP >> 4) * (uint32_t)k);
+                const uint32_t accum = (kbi > 0 || k > 0) ? 1u : 0u;
+                if constexpr (PAIR)
+                  umma_bf16_pair_warp(d_tmem, ad, bd, idesc, accum);
+                else
+                  umma_bf16_warp(d_tmem, ad, bd, idesc, accum);
+              }
+              (void)ad0;
+            } else if (nk == TC_BK / 16) {  // full k-block: one asm block of four MMAs
               const uint32_t accum = kbi > 0 ? 1u : 0u;
               if constexpr (PAIR)
                 umma4_pair_warp(d_tmem, ad0, bd0, idesc, accum, A_STEP >> 4, B_STEP >> 4);
