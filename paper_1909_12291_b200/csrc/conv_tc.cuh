@@ -875,6 +875,42 @@ struct DgradTcEpi {
 };
 
 // ------------------------------------------------------------------ wgrad
+// 32-channel wgrad (C % 64 == 32): A = x patches, MN-major, as four 32-wide
+// (tap, channel) blocks of 64 pixels per k-block (TMA im2col, SWIZZLE_64B, 4 KB
+// each); B = dY as in WgradTcLoader<2>. Replaces the cp.async gather.
+struct WgradTcLoader32 {
+  static constexpr int A_MN_MAJOR = 1, B_MN_MAJOR = 1;
+  static constexpr bool A_TMA_SW128 = false, A_SW64_MN = true, B_TMA_SW128 = true, PURE_TMA = true, KB2 = true;
+  CUtensorMap dmap, dmap3, xmap;
+  int slab3;
+  ConvGeom g;
+  int Kf, Mo, BN;
+  FastDiv d_ow, d_oh, d_c, d_k;
+  __device__ void init(uint8_t*, int, int) const {}
+  __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int, const uint8_t*,
+                       uint64_t* full) const {
+    uint32_t q, p, n, t;
+    d_ow.divmod((uint32_t)(kb * TC_BK), t, q);
+    d_oh.divmod(t, n, p);
+    int nblk = 0;
+#pragma unroll
+    for (int blk = 0; blk < 4; ++blk)
+      if (c.m0 + 32 * blk < Kf) ++nblk;
+    mbar_expect_tx(full, (uint32_t)BN * TC_BK * 2u + (uint32_t)nblk * 64u * 64u);
+    for (int blk = 0; blk < nblk; ++blk) {
+      uint32_t tap, c0, i, j;
+      d_c.divmod((uint32_t)(c.m0 + 32 * blk), tap, c0);
+      d_k.divmod(tap, i, j);
+      tma_load_im2col_4d(sA + blk * 4096, &xmap, (int)c0, (int)q * g.s, (int)p * g.s, (int)n, (uint16_t)j,
+                         (uint16_t)i, full);
+    }
+    if (slab3)
+      tma_load_3d(sB, &dmap3, 0, kb * TC_BK, c.n0 / 64, full);
+    else
+      for (int jb = 0; jb < BN / 64; ++jb) tma_load_2d(sB + jb * 8192, &dmap, c.n0 + 64 * jb, kb * TC_BK, full);
+  }
+};
+
 template <int MODE>
 struct WgradTcLoader {
   static constexpr bool TMA_B = MODE >= 1, IM2COL = MODE == 2;
@@ -1528,12 +1564,19 @@ inline int conv_wgrad_tc(const ConvGeom& g, const bf16* x, const bf16* dy, float
       ld.d_c = FastDiv(g.c); ld.d_k = FastDiv(g.k);
     };
     WgradTcLoader<2> ld2{};
+    WgradTcLoader32 ld32{};
     WgradTcLoader<1> ld1{};
     if (tma && g.c % 64 == 0 && !im2col_disabled() && make_tmap_mn64(&ld2.dmap, dy, Mo, g.co) &&
         make_tmap_im2col(&ld2.xmap, x, g, TC_BK)) {
       fill(ld2);
       ld2.slab3 = BN > 64 && make_tmap_mn64_slabs(&ld2.dmap3, dy, Mo, g.co, BN / 64) ? 1 : 0;
       e = tc_launch<BN>(ld2, ep, sh, num_sms, st);
+    } else if (tma && im2col32_ok(g) && make_tmap_mn64(&ld32.dmap, dy, Mo, g.co) &&
+               make_tmap_im2col(&ld32.xmap, x, g, TC_BK, 32)) {
+      ld32.g = g; ld32.Kf = Kf; ld32.Mo = Mo; ld32.BN = BN;
+      ld32.d_ow = FastDiv(g.ow); ld32.d_oh = FastDiv(g.oh); ld32.d_c = FastDiv(g.c); ld32.d_k = FastDiv(g.k);
+      ld32.slab3 = BN > 64 && make_tmap_mn64_slabs(&ld32.dmap3, dy, Mo, g.co, BN / 64) ? 1 : 0;
+      e = tc_launch<BN>(ld32, ep, sh, num_sms, st);
     } else if (tma && make_tmap_mn64(&ld1.dmap, dy, Mo, g.co)) {
       fill(ld1);
       e = tc_launch<BN>(ld1, ep, sh, num_sms, st);

@@ -356,6 +356,19 @@ CE_DEV uint64_t make_sdesc_sw64(uint32_t saddr) {
   return d;
 }
 
+// MN-major SWIZZLE_64B canonical layout (TMA box of 32 MN-elements x 64 K-rows):
+// K rows 64 B apart, 8-row K groups 512 B apart (SBO), 32-wide MN blocks LBO apart;
+// one 16-deep MMA K step advances the start address by 2 K groups (1,024 B).
+CE_DEV uint64_t make_sdesc_sw64_mn(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
 // MN-major SWIZZLE_128B canonical layout (TMA box of 64 MN-elements x 64 K-rows):
 // K rows 128 B apart, 8-row K groups 1024 B apart (SBO), 64-wide MN blocks LBO
 // apart; one 16-deep MMA K step advances the start address by 2 K groups.

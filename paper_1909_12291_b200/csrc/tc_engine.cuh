@@ -122,6 +122,13 @@ struct ASw64 : std::false_type {};
 template <class Loader>
 struct ASw64<Loader, std::void_t<decltype(Loader::A_SW64)>> : std::bool_constant<Loader::A_SW64> {};
 
+// Loader::A_SW64_MN: A is MN-major in 32-wide SWIZZLE_64B blocks of 64 K-rows (4 KB
+// apart): 32-channel im2col patches of the wgrad (C % 64 == 32)
+template <class Loader, class = void>
+struct ASw64Mn : std::false_type {};
+template <class Loader>
+struct ASw64Mn<Loader, std::void_t<decltype(Loader::A_SW64_MN)>> : std::bool_constant<Loader::A_SW64_MN> {};
+
 template <class Loader, class Epi>
 struct TcRoles {
   static constexpr int PW = ProducerWarps<Loader>::value;
@@ -516,12 +523,15 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
           // warp-converged issue (umma_*_warp): descriptors at K step 0, advanced linearly.
           // K-major SW128: +32 B per K=16 step; MN-major SW128: +2 K groups (2048 B);
           // no-swizzle K-major: +2 chunk columns (2 x rows x 16 B). Descriptor address field = bytes >> 4.
-          constexpr uint32_t A_STEP = Loader::A_TMA_SW128 ? (Loader::A_MN_MAJOR ? 2048u : 32u) : 2u * TC_BM * 16u;
+          constexpr uint32_t A_STEP = ASw64Mn<Loader>::value ? 1024u
+                                      : Loader::A_TMA_SW128 ? (Loader::A_MN_MAJOR ? 2048u : 32u)
+                                                            : 2u * TC_BM * 16u;
           constexpr uint32_t B_STEP = Loader::B_TMA_SW128 ? (Loader::B_MN_MAJOR ? 2048u : 32u) : 2u * BN * 16u;
           // one 64-deep k-block (planes h of the stage): MMAs over its nk K=16 steps
           auto kblock = [&](int h, int kbi, int nk) {
             const uint32_t pA = sA + (uint32_t)h * L::A_PLANE, pB = sB + (uint32_t)h * L::B_PLANE;
-            const uint64_t ad0 = Loader::A_TMA_SW128
+            const uint64_t ad0 = ASw64Mn<Loader>::value ? make_sdesc_sw64_mn(pA, 64 * 64)
+                                 : Loader::A_TMA_SW128
                                      ? (Loader::A_MN_MAJOR ? make_sdesc_sw128_mn(pA, 64 * 128) : make_sdesc_sw128(pA))
                                      : make_sdesc(pA, TC_BM * 16, 128);
             const uint64_t bd0 = Loader::B_TMA_SW128

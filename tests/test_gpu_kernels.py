@@ -21,7 +21,8 @@ torch = pytest.importorskip("torch")
 # (n, c, h, c_out, k, s): FIXED layers (c padded 3->8), SWEET-like, random-genome-like
 SHAPES = [(4, 8, 100, 32, 4, 2), (4, 32, 49, 64, 4, 1), (4, 64, 23, 128, 4, 1), (2, 256, 19, 256, 4, 1),
           (3, 16, 33, 8, 1, 2), (2, 8, 40, 24, 7, 3), (2, 128, 16, 256, 2, 3), (5, 64, 17, 16, 5, 2),
-          (2, 32, 12, 64, 3, 3), (1, 16, 9, 128, 6, 1), (2, 24, 11, 40, 3, 2)]
+          (2, 32, 12, 64, 3, 3), (1, 16, 9, 128, 6, 1), (2, 24, 11, 40, 3, 2),
+          (2, 96, 10, 64, 3, 1)]  # C % 64 == 32: the 32-channel (SWIZZLE_64B) im2col fwd / wgrad
 
 
 def _round(a, precision):
