@@ -25,9 +25,12 @@ inline bool col2im_dgrad_disabled() {  // CE_DISABLE_COL2IM=1: implicit dgrad ev
   }();
   return off;
 }
-// stride 1, few channels, N wide enough for 64-column TMA boxes
+// stride 1, few channels, N wide enough for 64-column TMA boxes. Since the
+// implicit dgrad's per-k-block cost came down (warp-converged MMA issue, two
+// k-blocks per stage, FastDiv decode) it wins from 32 input channels up:
+// FIXED's 32- and 64-channel layers took C1 from 404 to 322 us per step.
 inline bool col2im_dgrad_eligible(const ConvGeom& g) {
-  return g.s == 1 && g.c <= 64 && g.k >= 2 && g.k * g.k * g.c >= 64 && !col2im_dgrad_disabled();
+  return g.s == 1 && g.c < 32 && g.k >= 2 && g.k * g.k * g.c >= 64 && !col2im_dgrad_disabled();
 }
 
 // A = dY [M][C_out] K-major (128 x 64 SW128 boxes); B = W [C_out rows (K)][k*k*C_in (N)] MN-major
