@@ -241,6 +241,36 @@ struct PackedTcLoader {
     }
     return make_uint4(a.x, a.y, one, 0u);  // Kr % 8 == 4: last tap, then the ones column
   }
+  // forward (!MN): the register-pipelined fill (tc_engine SyncPipe); wgrad keeps load()
+  static constexpr bool PIPE = !MN;
+  struct Regs {
+    uint4 v[4];
+  };
+  __device__ void fetch(const TileCoord& c, int kb, int ptid, const uint8_t* table, Regs& rg) const {
+    const int* off = (const int*)table;
+    const int kcs = min(8, ((Kp - kb * TC_BK + 15) / 16) * 2);
+    const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;
+    const long long base = origin(c.m0 + r);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int kc = kc0 + 2 * e;
+      rg.v[e] = kc < kcs ? chunk(base, kb * TC_BK + kc * 8, off) : make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  __device__ void put(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const Regs& rg,
+                      uint64_t* full) const {
+    if (ptid == 0) {
+      mbar_expect_tx(full, (uint32_t)BN * 128u);
+      tma_load_2d(sB, &bmap, kb * TC_BK, c.n0, full);
+    }
+    const int kcs = min(8, ((Kp - kb * TC_BK + 15) / 16) * 2);
+    const int r = ptid & (TC_BM - 1), kc0 = ptid >> 7;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int kc = kc0 + 2 * e;
+      if (kc < kcs) st_shared_v4(sA + kmajor_off(TC_BM, r, kc), rg.v[e]);
+    }
+  }
   __device__ void load(const TileCoord& c, int kb, uint32_t sA, uint32_t sB, int ptid, const uint8_t* table,
                        uint64_t* full) const {
     const int* off = (const int*)table;

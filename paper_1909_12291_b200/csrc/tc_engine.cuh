@@ -85,6 +85,15 @@ struct SyncFill : std::false_type {};
 template <class Loader>
 struct SyncFill<Loader, std::void_t<decltype(Loader::SYNC_FILL)>> : std::bool_constant<Loader::SYNC_FILL> {};
 
+// Loader::PIPE (with SYNC_FILL): the fill is split into fetch() -> registers and
+// put() -> shared memory, and the producer fetches the NEXT k-block right after
+// putting the current one, so its global-load round trip overlaps the wait for a
+// free stage and the MMAs instead of being paid once per k-block.
+template <class Loader, class = void>
+struct SyncPipe : std::false_type {};
+template <class Loader>
+struct SyncPipe<Loader, std::void_t<decltype(Loader::PIPE)>> : std::bool_constant<Loader::PIPE> {};
+
 // Epi::EPI_WARPS_SYNC: epilogue warps when the loader fills stages with st.shared (SyncFill)
 template <class Epi, class = void>
 struct EpiWarpsSync {
@@ -327,6 +336,31 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     uint32_t phase = 0;
     int pending_stage[TC_MAX_LAG + 1];
     int npending = 0;
+    if constexpr (SyncPipe<Loader>::value) {  // register-pipelined st.shared fill
+      typename Loader::Regs regs;
+      int t = tile0, kb = 0;
+      TileCoord c = tile_at(t < total_tiles ? t : 0);
+      if (t < total_tiles) ld.fetch(c, c.kb0, ptid, table, regs);
+      while (t < total_tiles) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
+        const uint32_t sB = sA + L::A_BYTES;
+        ld.put(c, c.kb0 + kb, sA, sB, ptid, regs, &full[stage]);
+        fence_proxy_async();
+        mbar_arrive(&full[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++kb == c.nkb) {  // next k-block: this tile's, or the first of the next tile
+          kb = 0;
+          t += tstep;
+          if (t < total_tiles) c = tile_at(t);
+        }
+        if (t < total_tiles) ld.fetch(c, c.kb0 + kb, ptid, table, regs);
+      }
+      goto producer_done;
+    }
     for (int t = tile0; t < total_tiles; t += tstep) {
       TileCoord c = tile_at(t);
       for (int kb = 0; kb < c.nkb; kb += KPS) {
@@ -374,6 +408,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
     cp_async_wait_all();
     fence_proxy_async();
     for (int i = 0; i < npending; ++i) mbar_arrive(&full[pending_stage[i]]);
+  producer_done:
     if (threadIdx.x == 0) TC_TRACE_DONE(0);
   } else if (warp < R::MMA_WARP) {
     // ------------------------------------------------------------ epilogue
