@@ -257,6 +257,9 @@ def transfer_bytes(recs, genomes_by_id, splits, budget, datasets_uploaded):
 
 def main():
     args = parse_args()
+    if os.environ.get("CE_HANG_DUMP"):  # diagnostics: every thread's stack after N seconds (stderr)
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["CE_HANG_DUMP"]), repeat=True)
     rank, world, local = dist_env()
     # Libraries (ptxas, warnings) may print to stdout; the contract is ONE JSON
     # line there, so route fd 1 to stderr for the run.

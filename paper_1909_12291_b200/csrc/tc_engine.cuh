@@ -342,10 +342,13 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
       TileCoord c = tile_at(t < total_tiles ? t : 0);
       if (t < total_tiles) ld.fetch(c, c.kb0, ptid, table, regs);
       while (t < total_tiles) {
+        if (threadIdx.x == 0) TC_TRACE(0, 1, t, kb);
         mbar_wait(&empty[stage], phase ^ 1);
+        if (threadIdx.x == 0) TC_TRACE(0, 2, t, kb);
         const uint32_t sA = smem_base + stage * L::STAGE_BYTES;
         const uint32_t sB = sA + L::A_BYTES;
         ld.put(c, c.kb0 + kb, sA, sB, ptid, regs, &full[stage]);
+        if (threadIdx.x == 0) TC_TRACE(0, 7, t, kb);
         fence_proxy_async();
         mbar_arrive(&full[stage]);
         if (++stage == S) {
