@@ -436,11 +436,13 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
         // stored; two named register sets, no runtime-indexed arrays
         uint4* stage = (uint4*)(epi_stage + (warp - R::PW) * 1024);
         auto emit = [&](int col, uint32_t (&r)[16]) {
+          if (warp == R::PW && lane == 0) TC_TRACE(2, 9, t, col);
           float v[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
           uint32_t out[8];
           epi.convert(c, col, v, out);
+          if (warp == R::PW && lane == 0) TC_TRACE(2, 10, t, col);
           const int sw = (lane >> 2) & 1;
           stage[lane * 2 + sw] = make_uint4(out[0], out[1], out[2], out[3]);
           stage[lane * 2 + (sw ^ 1)] = make_uint4(out[4], out[5], out[6], out[7]);
@@ -452,6 +454,7 @@ __global__ void __launch_bounds__(TcRoles<Loader, Epi>::THREADS, 1)
             if (dst) *(uint4*)dst = stage[row * 2 + (half ^ ((row >> 2) & 1))];
           }
           __syncwarp();
+          if (warp == R::PW && lane == 0) TC_TRACE(2, 11, t, col);
         };
         uint32_t ra[16], rb[16];
         if (col_begin < col_end) tmem_ld16(tbase + col_begin, ra);

@@ -20,7 +20,7 @@ os.environ["CE_LIB"] = "trace"
 from paper_1909_12291_b200 import native  # noqa: E402
 
 KIND = {1: "prod_wait", 2: "prod_issue", 3: "mma_full", 4: "mma_acc_free", 5: "epi_start", 6: "epi_done",
-        7: "prod_loaded", 8: "mma_issued"}
+        7: "prod_loaded", 8: "mma_issued", 9: "epi_chunk", 10: "epi_converted", 11: "epi_stored"}
 
 
 def read_trace(lib):
