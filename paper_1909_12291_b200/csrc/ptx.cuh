@@ -28,7 +28,10 @@ CE_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"  // completed phase: no suspend round trip
+#ifdef CE_MBAR_SPIN  // experiment build: pure test_wait spin; measured slower (spinning warps take issue slots)
+#else
       "@!p mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+#endif
       "selp.b32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)

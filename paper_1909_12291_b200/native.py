@@ -108,7 +108,12 @@ _lock = threading.Lock()
 
 def library_path():
     # CE_LIB=trace: the -DCE_TC_TRACE debug build (tools/tc_trace.py), never the product
-    return _build.TRACE_LIB_PATH if os.environ.get("CE_LIB") == "trace" else _build.LIB_PATH
+    variant = os.environ.get("CE_LIB")
+    if variant == "trace":
+        return _build.TRACE_LIB_PATH
+    if variant:  # experiment builds: lib/libmenndl_sm100_<variant>.so (never the product)
+        return os.path.join(os.path.dirname(_build.LIB_PATH), f"libmenndl_sm100_{variant}.so")
+    return _build.LIB_PATH
 
 
 def load(build_if_missing=True):
@@ -118,9 +123,9 @@ def load(build_if_missing=True):
         if _lib is not None:
             return _lib
         path = library_path()
-        if path == _build.TRACE_LIB_PATH:
+        if path != _build.LIB_PATH:
             if not os.path.exists(path):
-                raise OSError(f"{path} missing; run python -m paper_1909_12291_b200.build --trace")
+                raise OSError(f"{path} missing (experiment build)")
         elif not os.path.exists(path) or (build_if_missing and not _build.up_to_date()):
             if not build_if_missing:
                 raise OSError(f"{path} missing; run python -m paper_1909_12291_b200.build")
